@@ -1,0 +1,165 @@
+/*
+ * helr_ckks.h — C ABI of the B200 RNS-CKKS evaluator behind the reference's
+ * evaluator protocol (helr.hesim.SimContext, pkg/src/helr/hesim.py:110-291).
+ *
+ * The reference is pure Python and binds no FFI; these entry points are what
+ * its evaluator methods become once a ciphertext is a real RNS polynomial pair
+ * on the device.  Each entry point cites the reference method it replaces.
+ *
+ * Conventions
+ *  - Plain C types only: device pointers are passed as (u)int64_t* living in
+ *    device memory (from torch tensors' data_ptr()), streams as void*
+ *    (cudaStream_t), sizes as int.  No entry point throws: each returns 0 on
+ *    success or a negative HELR_E* code, with a message retrievable through
+ *    helr_last_error().  Every call is asynchronous on the given stream.
+ *  - Ring: N = 2^log_n, primes[0..L-1] = q_0..q_{L-1} (ciphertext chain),
+ *    primes[L..L+K-1] = p_0..p_{K-1} (special primes, K = alpha =
+ *    ceil(L/dnum)).  All primes < 2^62, = 1 mod 2N.
+ *  - Polynomials are limb-major u64[limbs][N] of canonical residues in
+ *    [0, q), in negacyclic NTT (evaluation) form unless stated otherwise.
+ *    NTT slot i holds a(psi^(2*brv(i)+1)).
+ *  - A ciphertext buffer is u64[2][L][N] (c0 limbs, then c1 limbs, always
+ *    sized for the top level).  "level" l means limbs 0..l are active; the
+ *    rest of the buffer is ignored.  A batch is `count` such buffers back to
+ *    back (stride 2*L*N words).
+ *  - Secret key buffer: u64[L+K][N] (NTT form over every prime).
+ *  - Switching key (relinearisation or Galois): u64[beta][2][L+K][N] with
+ *    beta = ceil(L/alpha) digits of the top-level chain.
+ *  - Randomness is a counter-based generator keyed by (seed, stream, index)
+ *    so device and CPU oracle produce identical keys and ciphertexts.
+ */
+#ifndef HELR_CKKS_H
+#define HELR_CKKS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HELR_OK 0
+#define HELR_EINVAL (-1)
+#define HELR_ECUDA (-2)
+#define HELR_ENOMEM (-3)
+
+typedef struct helr_ctx helr_ctx;
+
+/* Last error message of the calling thread (empty when none). */
+int helr_last_error(char* buf, size_t len);
+
+/* Library/ABI version (major*10000 + minor*100 + patch). */
+int helr_version(void);
+
+/* Context: builds twiddle, basis-conversion and rescale tables on the device.
+ * Replaces SimContext.__init__ (hesim.py:119-122) at ring level.  max_batch
+ * sizes the key-switching workspace (ciphertexts per batched call). */
+int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum,
+                    const uint64_t* primes, const uint64_t* psi, int cbd_eta,
+                    int max_batch);
+int helr_ctx_destroy(helr_ctx* ctx);
+
+/* ---- ring primitives (primitive sweep; building blocks) ---------------- */
+
+/* In-place forward / inverse negacyclic NTT of `count` polynomials, each with
+ * n_limbs limbs using primes first_prime .. first_prime+n_limbs-1; polynomial
+ * b limb i lives at data + b*poly_stride + i*N. */
+int helr_ntt_fwd(helr_ctx* ctx, uint64_t* data, int first_prime, int n_limbs,
+                 int count, int64_t poly_stride, void* stream);
+int helr_ntt_inv(helr_ctx* ctx, uint64_t* data, int first_prime, int n_limbs,
+                 int count, int64_t poly_stride, void* stream);
+
+/* ---- keys (client side; not in the reference, which has no keys) ------- */
+
+int helr_keygen_secret(helr_ctx* ctx, uint64_t* sk, uint64_t seed, void* stream);
+/* galois == 0: relinearisation key (s^2 -> s); otherwise key for X -> X^galois. */
+int helr_keygen_switch(helr_ctx* ctx, const uint64_t* sk, int64_t galois,
+                       uint64_t* evk, uint64_t seed, uint64_t key_id, void* stream);
+
+/* ---- encryption boundary (SimContext.enc / dec, hesim.py:146-162) ------- */
+
+/* Encode-side integers -> ciphertexts.  msg: int64[count][N] integer
+ * coefficients (already scaled and rounded on the host); ciphertext b uses
+ * randomness stream id first_ct_id + b. */
+int helr_encrypt(helr_ctx* ctx, const uint64_t* sk, const int64_t* msg,
+                 uint64_t* ct, int count, int level, uint64_t seed,
+                 uint64_t first_ct_id, void* stream);
+/* Decrypt through q_0 only: out[b][n] = centred coefficient n of
+ * (c0 + c1*s) mod q_0 (valid while |m| < q_0/2). */
+int helr_decrypt(helr_ctx* ctx, const uint64_t* sk, const uint64_t* ct,
+                 int count, int level, int64_t* out, void* stream);
+/* Integer polynomial -> plaintext in NTT form over limbs 0..level. */
+int helr_encode_plain(helr_ctx* ctx, const int64_t* msg, uint64_t* pt,
+                      int count, int level, void* stream);
+
+/* ---- arithmetic (SimContext.add/cadd/mul/cmul/imul, hesim.py:166-216) -- */
+
+int helr_add(helr_ctx* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out,
+             int count, int level, void* stream);
+int helr_sub(helr_ctx* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out,
+             int count, int level, void* stream);
+/* c0 += c (a constant polynomial); c: u64[level+1] residues (cadd, scalar). */
+int helr_add_const(helr_ctx* ctx, const uint64_t* a, const uint64_t* c,
+                   uint64_t* out, int count, int level, void* stream);
+/* c0 += pt (cadd, vector); pt: u64[L][N] NTT plaintext. */
+int helr_add_plain(helr_ctx* ctx, const uint64_t* a, const uint64_t* pt,
+                   uint64_t* out, int count, int level, void* stream);
+/* Both polynomials times a per-limb constant c (u64[level+1]); no rescale. */
+int helr_mul_const(helr_ctx* ctx, const uint64_t* a, const uint64_t* c,
+                   uint64_t* out, int count, int level, void* stream);
+/* Both polynomials times an NTT plaintext; no rescale. */
+int helr_mul_plain(helr_ctx* ctx, const uint64_t* a, const uint64_t* pt,
+                   uint64_t* out, int count, int level, void* stream);
+/* Drop q_level: out (level-1) = round(in / q_level). */
+int helr_rescale(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count,
+                 int level, void* stream);
+/* ct x ct product with relinearisation (no rescale): out = relin(a*b). */
+int helr_mul_relin(helr_ctx* ctx, const uint64_t* a, const uint64_t* b,
+                   const uint64_t* rlk, uint64_t* out, int count, int level,
+                   void* stream);
+/* Multiply by X^(N/2) (slots * i). */
+int helr_imul(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count,
+              int level, void* stream);
+
+/* ---- rotations (SimContext.rotate, sum_col_vec, sum_rows) --------------- */
+
+/* out = rot_galois(a).  With accumulate != 0: out = a + rot_galois(a)
+ * (the rotate-and-add step of hesim.py:255-264, 278-280).  All `count`
+ * ciphertexts share one read of the key. */
+int helr_rotate(helr_ctx* ctx, const uint64_t* a, int64_t galois,
+                const uint64_t* gk, uint64_t* out, int count, int level,
+                int accumulate, void* stream);
+
+/* ---- refresh stand-in (SimContext.bootstrap, hesim.py:228-236) ---------- */
+
+/* NOT bootstrapping: decrypts through q_0 with the secret key, multiplies the
+ * integer message by `ratio` (fp64, round-to-nearest; 1.0 keeps it exact) and
+ * re-encrypts at `out_level` with fresh randomness (stream first_ct_id + b). */
+int helr_refresh(helr_ctx* ctx, const uint64_t* sk, const uint64_t* a,
+                 int in_level, double ratio, uint64_t* out, int out_level,
+                 int count, uint64_t seed, uint64_t first_ct_id, void* stream);
+
+/* ---- fused training step (enctrain.py:344-398 loop body) ---------------- */
+
+/* One enhanced-NAG iteration over one batch of `blocks` Z ciphertexts (one
+ * column block), depth-7 schedule.  All constants are
+ * per-limb residues prepared by the host planner:
+ *   consts: u64[HELR_NAG_NCONST][L] (see DESIGN.md for the order)
+ *   mask_pt: u64[L][N] row-start mask plaintext (NTT form)
+ *   rot_keys: device pointers to the Galois keys, left steps 1..g/2, right
+ *   steps 1..g/2, row steps g..S/2 (in that order).
+ * w, v: in/out weight ciphertexts (level lw in, level lw-7 out).
+ * bbar: quadratic-gradient scale ciphertext at level >= lw-5. */
+#define HELR_NAG_NCONST 10
+int helr_nag_iteration(helr_ctx* ctx, const uint64_t* z, int blocks, int log_g,
+                       int log_m, const uint64_t* w, const uint64_t* v,
+                       const uint64_t* bbar, int bbar_level, int lw,
+                       const uint64_t* rlk, const uint64_t* const* rot_keys,
+                       const uint64_t* mask_pt, const uint64_t* consts,
+                       uint64_t* w_out, uint64_t* v_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HELR_CKKS_H */

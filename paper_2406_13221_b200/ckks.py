@@ -1,0 +1,438 @@
+"""``GpuContext``: the reference evaluator protocol over real RNS-CKKS on one
+B200.
+
+Drop-in for ``helr.hesim.SimContext`` (hesim.py:110-291): the same method
+names and argument meaning (``enc``, ``dec``, ``add``, ``cadd``, ``mul``,
+``cmul``, ``imul``, ``rotate``, ``bootstrap``, ``sum_col_vec``,
+``sum_rows``), the same ``counters`` / ``reset_counters`` ledger surface
+(hesim.py:117-128), the same errors (``ValueError`` for scale mismatch,
+oversize messages, bad constant shapes and layouts; ``NeedsBootstrap`` when
+an operation would leave fewer than ``log_delta`` bits, hesim.py:136-142),
+and ciphertext handles exposing ``level_bits`` / ``scale_bits`` /
+``boot_count`` (hesim.py:93-107).  Values are immutable: every operation
+returns a new handle owning a fresh device buffer.
+
+Under the surface each handle is a u64[2][L][N] device buffer in NTT form.
+Every call goes straight to the sm_100a library through the C ABI
+(include/helr_ckks.h); there is no CPU fallback.
+
+Scale management.  Each handle carries its exact fp64 scale.  Fresh
+encryptions use Delta_top = 2**scale_bits; ct x ct products of operands at
+level l land on Delta_{l-1} = Delta_l**2 / q_l; constant products encode the
+constant at Delta_{l-1} * q_l / scale so they land on the same canonical
+scale.  Two handles at one level therefore always share a scale, and an
+``add`` of handles at different levels first brings the higher one down
+with an exact-scale constant product (the result level is the minimum, as
+in hesim.py:172-173).
+
+Level accounting: one rescale drops one limb = ``scale_bits`` bits, so
+``level_bits`` follows the reference arithmetic with
+log_delta == log_delta_c == scale_bits (see params.py).
+"""
+
+from __future__ import annotations
+
+import weakref
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .encoder import Encoder
+from .params import CkksParams
+
+__all__ = ["GpuContext", "GpuCiphertext", "NeedsBootstrap"]
+
+
+class NeedsBootstrap(Exception):
+    """Raised when an operation would leave too little modulus to decrypt
+    (mirrors helr.hesim.NeedsBootstrap, hesim.py:37-38)."""
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class GpuCiphertext:
+    """Handle to one device ciphertext (u64[2][L][N], NTT form)."""
+
+    __slots__ = ("data", "level", "scale", "scale_bits", "boot_count", "_ctx", "__weakref__")
+
+    def __init__(self, ctx: "GpuContext", data: torch.Tensor, level: int, scale: float,
+                 scale_bits: int, boot_count: int = 0):
+        self._ctx = weakref.ref(ctx)
+        self.data = data
+        self.level = int(level)
+        self.scale = float(scale)
+        self.scale_bits = int(scale_bits)
+        self.boot_count = int(boot_count)
+
+    @property
+    def level_bits(self) -> int:
+        return self._ctx().ckks.level_bits(self.level)
+
+    @property
+    def slots(self) -> np.ndarray:
+        """Decrypted slots (test-harness privilege; does not touch counters)."""
+        return self._ctx()._decrypt_slots(self)
+
+    def __repr__(self) -> str:
+        return f"GpuCiphertext(level={self.level}, level_bits={self.level_bits}, scale=2^{np.log2(self.scale):.6f})"
+
+
+class GpuContext:
+    """RNS-CKKS evaluator bound to one parameter set and one secret key.
+
+    ``seed`` drives every random draw (secret key, switching keys,
+    encryption randomness) through the counter-based generator shared with
+    the CPU oracle, so a given seed reproduces the same residues there.
+    """
+
+    COUNTER_KEYS = ("enc", "dec", "add", "cadd", "mul", "cmul", "imul", "rotate", "bootstrap")
+
+    def __init__(self, ckks: CkksParams, seed: int = 0, noise_sigma: float = 1e-7,
+                 device: Optional[str] = None, max_batch: int = 8):
+        if not torch.cuda.is_available():
+            raise _lib.NativeLibraryError("GpuContext needs a CUDA device (no CPU fallback)")
+        self.ckks = ckks
+        self.params = ckks.he_params(noise_sigma=noise_sigma, seed=seed)
+        self.device = torch.device(device or "cuda")
+        self.encoder = Encoder(ckks.log_n)
+        self.seed = int(seed)
+        self.key_seed = (self.seed << 1) | 1
+        self.enc_seed = (self.seed << 1) + 2
+        self.counters = dict.fromkeys(self.COUNTER_KEYS, 0)
+        self._next_ct_id = 1
+        self.max_batch = max_batch
+        self._lib = _lib.load()
+        primes = (ctypes_u64 * len(ckks.primes))(*ckks.primes)
+        psi = (ctypes_u64 * len(ckks.psi))(*ckks.psi)
+        handle = ctypes_vp()
+        with torch.cuda.device(self.device):
+            _lib.check(self._lib.helr_ctx_create(ctypes_byref(handle), ckks.log_n, ckks.L, ckks.K, ckks.dnum,
+                                                 primes, psi, ckks.cbd_eta, max_batch), "helr_ctx_create")
+        self._h = handle
+        self._residue_cache: dict = {}
+        self.sk = self._empty((ckks.L + ckks.K, ckks.n))
+        self._call("helr_keygen_secret", _ptr(self.sk), self.key_seed, _stream())
+        self.rlk = self._switch_key(0)
+        self._gks: dict[int, torch.Tensor] = {}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                torch.cuda.synchronize(self.device)
+                self._lib.helr_ctx_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ------------------------------------------------------------------ infra
+    @property
+    def handle(self):
+        return self._h
+
+    def _call(self, name: str, *args) -> None:
+        _lib.check(getattr(self._lib, name)(self._h, *args), name)
+
+    def _empty(self, shape) -> torch.Tensor:
+        return torch.empty(shape, dtype=torch.int64, device=self.device)
+
+    def _ct_buffer(self, count: int = 0) -> torch.Tensor:
+        shape = (2, self.ckks.L, self.ckks.n) if count == 0 else (count, 2, self.ckks.L, self.ckks.n)
+        return self._empty(shape)
+
+    def _wrap(self, data, level, scale, boot_count=0) -> GpuCiphertext:
+        return GpuCiphertext(self, data, level, scale, self.params.log_delta, boot_count)
+
+    def _switch_key(self, galois: int) -> torch.Tensor:
+        ck = self.ckks
+        beta = -(-ck.L // ck.alpha)
+        evk = self._empty((beta, 2, ck.L + ck.K, ck.n))
+        self._call("helr_keygen_switch", _ptr(self.sk), int(galois), _ptr(evk), self.key_seed, int(galois), _stream())
+        return evk
+
+    def galois_key(self, galois: int) -> torch.Tensor:
+        g = int(galois) % (2 * self.ckks.n)
+        if g not in self._gks:
+            self._gks[g] = self._switch_key(g)
+        return self._gks[g]
+
+    def galois_for_rotation(self, k: int) -> int:
+        s = self.ckks.slots
+        return pow(5, k % s, 2 * self.ckks.n)
+
+    def reset_counters(self) -> dict:
+        """Return the current counts and zero them (hesim.py:124-128)."""
+        snapshot = dict(self.counters)
+        self.counters = dict.fromkeys(self.COUNTER_KEYS, 0)
+        return snapshot
+
+    def _take_ct_ids(self, count: int) -> int:
+        first = self._next_ct_id
+        self._next_ct_id += count
+        return first
+
+    def _residues(self, value: int, level: int) -> torch.Tensor:
+        """Per-limb residues of an integer constant, as a device vector."""
+        key = (int(value), level)
+        t = self._residue_cache.get(key)
+        if t is None:
+            res = [int(value) % q for q in self.ckks.q[: level + 1]]
+            t = torch.tensor(np.array(res, dtype=np.uint64).view(np.int64), device=self.device)
+            if len(self._residue_cache) > 4096:
+                self._residue_cache.clear()
+            self._residue_cache[key] = t
+        return t
+
+    def _plain(self, coef: np.ndarray, level: int) -> torch.Tensor:
+        ck = self.ckks
+        msg = torch.from_numpy(np.ascontiguousarray(coef, dtype=np.int64)).to(self.device)
+        pt = self._empty((ck.L, ck.n))
+        self._call("helr_encode_plain", _ptr(msg), _ptr(pt), 1, level, _stream())
+        return pt
+
+    def _spend(self, level_bits: int, cost: int, op: str) -> None:
+        remaining = level_bits - cost
+        if remaining < self.params.log_delta:
+            raise NeedsBootstrap(f"{op} needs {cost + self.params.log_delta} bits but only {level_bits} remain")
+
+    # --------------------------------------------------------- encryption
+    def encrypt_coefficients(self, coef: np.ndarray, scale: float, level: Optional[int] = None) -> list:
+        """Encrypt a batch of integer polynomials (int64[B][N]) at ``level``."""
+        ck = self.ckks
+        level = ck.top_level if level is None else level
+        coef = np.ascontiguousarray(np.atleast_2d(coef), dtype=np.int64)
+        count = coef.shape[0]
+        buf = self._ct_buffer(count)
+        msg = torch.from_numpy(coef).to(self.device)
+        first = self._take_ct_ids(count)
+        self._call("helr_encrypt", _ptr(self.sk), _ptr(msg), _ptr(buf), count, level, self.enc_seed, first, _stream())
+        return [self._wrap(buf[b], level, scale) for b in range(count)]
+
+    def enc(self, message) -> GpuCiphertext:
+        """Encrypt at most N/2 values, zero-padded (hesim.py:146-158)."""
+        m = np.asarray(message, dtype=np.complex128).ravel()
+        if m.shape[0] > self.ckks.slots:
+            raise ValueError(f"message has {m.shape[0]} slots, maximum is {self.ckks.slots}")
+        scale = self.ckks.level_scales[self.ckks.top_level]
+        coef = self.encoder.encode(m, scale)
+        self.counters["enc"] += 1
+        return self.encrypt_coefficients(coef, scale)[0]
+
+    def enc_many(self, messages) -> list:
+        """Batched ``enc`` of a (B, <=S) array; one device call."""
+        msgs = np.atleast_2d(np.asarray(messages, dtype=np.complex128))
+        if msgs.shape[1] > self.ckks.slots:
+            raise ValueError(f"message has {msgs.shape[1]} slots, maximum is {self.ckks.slots}")
+        scale = self.ckks.level_scales[self.ckks.top_level]
+        coef = self.encoder.encode(msgs, scale)
+        self.counters["enc"] += msgs.shape[0]
+        return self.encrypt_coefficients(coef, scale)
+
+    def decrypt_coefficients(self, ct: GpuCiphertext) -> np.ndarray:
+        out = self._empty((1, self.ckks.n))
+        self._call("helr_decrypt", _ptr(self.sk), _ptr(ct.data), 1, ct.level, _ptr(out), _stream())
+        return out.cpu().numpy()[0]
+
+    def _decrypt_slots(self, ct: GpuCiphertext) -> np.ndarray:
+        return self.encoder.decode(self.decrypt_coefficients(ct), ct.scale)
+
+    def dec(self, ct: GpuCiphertext) -> np.ndarray:
+        """Decrypted, decoded slots as complex128[N/2] (hesim.py:160-162)."""
+        self.counters["dec"] += 1
+        return self._decrypt_slots(ct)
+
+    # --------------------------------------------------------- level moves
+    def _drop_to(self, ct: GpuCiphertext, level: int, scale: float) -> GpuCiphertext:
+        """Bring ``ct`` down to ``level`` (< ct.level) landing exactly on ``scale``:
+        integer constant round(scale * q_{level+1} / ct.scale), then rescale."""
+        if level >= ct.level:
+            raise ValueError("can only move a ciphertext down")
+        ck = self.ckks
+        top = level + 1
+        factor = int(np.rint(scale * float(ck.q[top]) / ct.scale))
+        tmp = self._ct_buffer()
+        self._call("helr_mul_const", _ptr(ct.data), _ptr(self._residues(factor, top)), _ptr(tmp), 1, top, _stream())
+        out = self._ct_buffer()
+        self._call("helr_rescale", _ptr(tmp), _ptr(out), 1, top, _stream())
+        exact = ct.scale * factor / float(ck.q[top])
+        return self._wrap(out, level, exact, ct.boot_count)
+
+    def _align(self, a: GpuCiphertext, b: GpuCiphertext):
+        if a.level > b.level:
+            a = self._drop_to(a, b.level, b.scale)
+        elif b.level > a.level:
+            b = self._drop_to(b, a.level, a.scale)
+        if abs(a.scale / b.scale - 1.0) > 1e-9:
+            raise ValueError(f"exact scale mismatch at level {a.level}: {a.scale} vs {b.scale}")
+        return a, b
+
+    # --------------------------------------------------------- arithmetic
+    def add(self, a: GpuCiphertext, b: GpuCiphertext) -> GpuCiphertext:
+        if a.scale_bits != b.scale_bits:
+            raise ValueError(f"scale mismatch: {a.scale_bits} vs {b.scale_bits}")
+        a, b = self._align(a, b)
+        self.counters["add"] += 1
+        out = self._ct_buffer()
+        self._call("helr_add", _ptr(a.data), _ptr(b.data), _ptr(out), 1, a.level, _stream())
+        return self._wrap(out, a.level, a.scale, max(a.boot_count, b.boot_count))
+
+    def _const_vector(self, const):
+        c = np.asarray(const, dtype=np.complex128)
+        if c.ndim == 0:
+            return c
+        if c.shape != (self.ckks.slots,):
+            raise ValueError(f"constant vector has shape {c.shape}, expected ({self.ckks.slots},)")
+        return c
+
+    def cadd(self, a: GpuCiphertext, const) -> GpuCiphertext:
+        c = self._const_vector(const)
+        self.counters["cadd"] += 1
+        out = self._ct_buffer()
+        if c.ndim == 0 and c.imag == 0:
+            k = self.encoder.encode_constant(c.real, a.scale)
+            self._call("helr_add_const", _ptr(a.data), _ptr(self._residues(k, a.level)), _ptr(out), 1, a.level,
+                       _stream())
+        else:
+            vec = np.full(self.ckks.slots, c) if c.ndim == 0 else c
+            pt = self._plain(self.encoder.encode(vec, a.scale), a.level)
+            self._call("helr_add_plain", _ptr(a.data), _ptr(pt), _ptr(out), 1, a.level, _stream())
+        return self._wrap(out, a.level, a.scale, a.boot_count)
+
+    def mul(self, a: GpuCiphertext, b: GpuCiphertext) -> GpuCiphertext:
+        """Slotwise product, relinearised and rescaled: one limb (hesim.py:186-195)."""
+        self._spend(min(a.level_bits, b.level_bits), self.params.log_delta, "mul")
+        self.counters["mul"] += 1
+        if a.level != b.level:
+            if a.level > b.level:
+                a = self._drop_to(a, b.level, self.ckks.level_scales[b.level])
+            else:
+                b = self._drop_to(b, a.level, self.ckks.level_scales[a.level])
+        lvl = a.level
+        tmp = self._ct_buffer()
+        self._call("helr_mul_relin", _ptr(a.data), _ptr(b.data), _ptr(self.rlk), _ptr(tmp), 1, lvl, _stream())
+        out = self._ct_buffer()
+        self._call("helr_rescale", _ptr(tmp), _ptr(out), 1, lvl, _stream())
+        scale = a.scale * b.scale / float(self.ckks.q[lvl])
+        return self._wrap(out, lvl - 1, scale, max(a.boot_count, b.boot_count))
+
+    def cmul(self, a: GpuCiphertext, const) -> GpuCiphertext:
+        """Product with a public constant, landing on the canonical scale of
+        the next level (hesim.py:197-206)."""
+        self._spend(a.level_bits, self.params.log_delta_c, "cmul")
+        c = self._const_vector(const)
+        self.counters["cmul"] += 1
+        ck = self.ckks
+        lvl = a.level
+        target = ck.level_scales[lvl - 1]
+        factor = target * float(ck.q[lvl]) / a.scale
+        tmp = self._ct_buffer()
+        if c.ndim == 0 and c.imag == 0:
+            k = self.encoder.encode_constant(c.real, factor)
+            self._call("helr_mul_const", _ptr(a.data), _ptr(self._residues(k, lvl)), _ptr(tmp), 1, lvl, _stream())
+        else:
+            vec = np.full(ck.slots, c) if c.ndim == 0 else c
+            pt = self._plain(self.encoder.encode(vec, factor), lvl)
+            self._call("helr_mul_plain", _ptr(a.data), _ptr(pt), _ptr(tmp), 1, lvl, _stream())
+        out = self._ct_buffer()
+        self._call("helr_rescale", _ptr(tmp), _ptr(out), 1, lvl, _stream())
+        return self._wrap(out, lvl - 1, target, a.boot_count)
+
+    def imul(self, a: GpuCiphertext) -> GpuCiphertext:
+        """Multiply by i: X^(N/2), exact and free of level (hesim.py:208-216)."""
+        self.counters["imul"] += 1
+        out = self._ct_buffer()
+        self._call("helr_imul", _ptr(a.data), _ptr(out), 1, a.level, _stream())
+        return self._wrap(out, a.level, a.scale, a.boot_count)
+
+    def rotate(self, a: GpuCiphertext, k: int) -> GpuCiphertext:
+        """Cyclic left rotation by k slots; negative k rotates right (hesim.py:218-226)."""
+        self.counters["rotate"] += 1
+        return self._rotate(a, k, accumulate=False)
+
+    def _rotate(self, a: GpuCiphertext, k: int, accumulate: bool) -> GpuCiphertext:
+        kk = int(k) % self.ckks.slots
+        out = self._ct_buffer()
+        if kk == 0:
+            if accumulate:
+                self._call("helr_add", _ptr(a.data), _ptr(a.data), _ptr(out), 1, a.level, _stream())
+            else:
+                out.copy_(a.data)
+            return self._wrap(out, a.level, a.scale, a.boot_count)
+        g = self.galois_for_rotation(kk)
+        self._call("helr_rotate", _ptr(a.data), g, _ptr(self.galois_key(g)), _ptr(out), 1, a.level,
+                   1 if accumulate else 0, _stream())
+        return self._wrap(out, a.level, a.scale, a.boot_count)
+
+    def rotate_add(self, a: GpuCiphertext, k: int) -> GpuCiphertext:
+        """a + rotate(a, k) in one fused key switch (counts as rotate + add)."""
+        self.counters["rotate"] += 1
+        self.counters["add"] += 1
+        return self._rotate(a, k, accumulate=True)
+
+    def bootstrap(self, ct: GpuCiphertext) -> GpuCiphertext:
+        """Refresh STAND-IN (not bootstrapping): decrypt through q_0 with the
+        secret key, rescale the integer message to the top-level scale and
+        re-encrypt at the top level (hesim.py:228-236 semantics: level back
+        to log_q, slots preserved)."""
+        self.counters["bootstrap"] += 1
+        ck = self.ckks
+        top = ck.top_level
+        target = ck.level_scales[top]
+        ratio = target / ct.scale
+        out = self._ct_buffer()
+        first = self._take_ct_ids(1)
+        self._call("helr_refresh", _ptr(self.sk), _ptr(ct.data), ct.level, float(ratio), _ptr(out), top, 1,
+                   self.enc_seed, first, _stream())
+        return self._wrap(out, top, target, ct.boot_count + 1)
+
+    # ------------------------------------------------------ structured sums
+    def sum_col_vec(self, a: GpuCiphertext, layout) -> GpuCiphertext:
+        """Per-row sums replicated across each row (hesim.py:240-265): log2 g
+        rotate-and-add steps left, the row-start mask (one cmul), log2 g steps
+        right.  Each rotate-and-add is one fused key switch."""
+        m, g = layout.m, layout.g
+        if m * g != self.ckks.slots:
+            raise ValueError(f"layout {m}x{g} does not fill {self.ckks.slots} slots")
+        if g == 1:
+            return a
+        acc = a
+        step = 1
+        while step < g:
+            acc = self.rotate_add(acc, step)
+            step *= 2
+        mask = np.zeros(self.ckks.slots)
+        mask[::g] = 1.0
+        acc = self.cmul(acc, mask)
+        step = 1
+        while step < g:
+            acc = self.rotate_add(acc, -step)
+            step *= 2
+        return acc
+
+    def sum_rows(self, a: GpuCiphertext, layout) -> GpuCiphertext:
+        """Per-column sums over all m rows, already replicated (hesim.py:267-281)."""
+        m, g = layout.m, layout.g
+        if m * g != self.ckks.slots:
+            raise ValueError(f"layout {m}x{g} does not fill {self.ckks.slots} slots")
+        acc = a
+        step = g
+        while step < m * g:
+            acc = self.rotate_add(acc, step)
+            step *= 2
+        return acc
+
+
+# ctypes helpers (kept local to avoid importing ctypes names everywhere)
+import ctypes as _ct  # noqa: E402
+
+ctypes_u64 = _ct.c_uint64
+ctypes_vp = _ct.c_void_p
+ctypes_byref = _ct.byref

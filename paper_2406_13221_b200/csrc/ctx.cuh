@@ -1,0 +1,76 @@
+// ctx.cuh — device context: ring tables and key-switching workspace.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "modarith.cuh"
+
+#define HELR_MAXP 64
+
+// Per-prime scalar tables, passed by value to kernels (all device pointers).
+struct Tables {
+    const u64* q;        // [LK]
+    const u64* br1;      // floor(2^128/q) high word
+    const u64* br0;      // low word
+    const u64* tw;       // [LK][N]  psi^brv(k)
+    const u64* tw_sh;
+    const u64* itw;      // [LK][N]  psi^-brv(k)
+    const u64* itw_sh;
+    const u64* ninv;     // [LK]  N^-1
+    const u64* ninv_sh;
+    const u64* itw1n;    // [LK]  psi^-brv(1) * N^-1  (last inverse stage)
+    const u64* itw1n_sh;
+    int log_n, n, L, K, alpha, beta;
+};
+
+// Limb selection for batched kernels: limb i of item z lives at
+// base + z*item_stride + off[i]*N and uses prime prime[i].
+struct LimbMap {
+    int count;
+    unsigned char off[HELR_MAXP];
+    unsigned char prime[HELR_MAXP];
+};
+
+struct helr_ctx {
+    int log_n, n, L, K, LK, dnum, alpha, beta, eta, max_batch;
+    std::vector<u64> primes, psi;
+    Tables t;
+    // raw device allocations of the tables
+    u64* d_tab = nullptr;
+    size_t tab_words = 0;
+    // rescale: qlinv[l*L + i] = q_l^-1 mod q_i (+ shoup), l >= 1, i < l
+    const u64* qlinv = nullptr;
+    const u64* qlinv_sh = nullptr;
+    // ModUp: per (level l, digit j): offset into modup table
+    std::vector<size_t> modup_off;  // [L * beta]
+    const u64* modup = nullptr;     // packed, see ctx.cu
+    size_t* d_modup_offs = nullptr; // device copy of modup_off
+    // ModDown (level-independent)
+    const u64* md_phinv = nullptr;     // [K]   (P/p_k)^-1 mod p_k
+    const u64* md_phinv_sh = nullptr;
+    const u64* md_phmod = nullptr;     // [K][L] (P/p_k) mod q_i
+    const u64* md_phmod_sh = nullptr;
+    const u64* md_pinv = nullptr;      // [L] P^-1 mod q_i
+    const u64* md_pinv_sh = nullptr;
+    const u64* pmod = nullptr;         // [L] P mod q_i
+    const u64* imul_f = nullptr;       // [L][N] NTT of X^(N/2)
+    // key-switching workspace
+    u64* ws = nullptr;
+    size_t ws_words = 0;
+};
+
+void set_error(const std::string& msg);
+bool cuda_ok(cudaError_t e, const char* what);
+
+// helpers shared by the .cu files
+inline LimbMap limb_range(int first_prime, int count, int first_off = 0) {
+    LimbMap m;
+    m.count = count;
+    for (int i = 0; i < count; i++) {
+        m.off[i] = (unsigned char)(first_off + i);
+        m.prime[i] = (unsigned char)(first_prime + i);
+    }
+    return m;
+}

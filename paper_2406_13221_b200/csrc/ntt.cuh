@@ -1,0 +1,273 @@
+// ntt.cuh — negacyclic NTT passes for sm_100a.
+//
+// Forward: Cooley-Tukey over bit-reversed powers of psi with Harvey lazy
+// butterflies (values in [0, 4q)); output slot i = a(psi^(2 brv(i) + 1)).
+// Inverse: Gentleman-Sande with psi^-1, lazy in [0, 2q), N^-1 folded into
+// the last stage.  Both equal, residue for residue, the oracle's loops.
+//
+// Decomposition.  log N = s1 + s2.  The first s1 forward stages only mix
+// elements with equal index mod 2^s2 ("columns", stride 2^s2); the last s2
+// stages only mix within contiguous blocks of 2^s2 ("rows").  Each pass is
+// one kernel holding T = 2^LOG_T elements per sub-transform in registers
+// (R = 2^LOG_R per thread, radix-R register stages) and exchanging through
+// shared memory between register groups, so a limb is read and written
+// once per pass.  N <= 2^11 runs as a single row pass.  Column passes put
+// COLS adjacent columns in one CTA so every global access is a 128-byte
+// segment; row passes put COLS contiguous blocks in one CTA.
+//
+// Loader / Storer functors give each pass its prologue / epilogue, so
+// rescale, ModUp and ModDown fuse their basis conversions into the NTT
+// instead of making extra passes over HBM.
+#pragma once
+#include "ctx.cuh"
+
+struct NttPassArgs {
+    int log_n;
+    int st0;        // first global stage of this pass (forward numbering)
+    int final_out;  // 1: reduce outputs to [0, q)
+};
+
+template <int LOG_T, int LOG_R>
+struct NttShape {
+    static constexpr int T = 1 << LOG_T;
+    static constexpr int R = 1 << LOG_R;
+    static constexpr int NG = (LOG_T + LOG_R - 1) / LOG_R;
+};
+
+// insert LOG_R zero bits at bit position lo of s
+__device__ __forceinline__ int spread_index(int s, int lo, int log_r) {
+    return ((s >> lo) << (lo + log_r)) | (s & ((1 << lo) - 1));
+}
+
+// Loader: u64 operator()(int z, int li, int prime, int off) const
+// Storer: void operator()(int z, int li, int prime, int off, u64 v) const
+// grid: x = sub-transform tiles, y = limb index in map, z = batch item.
+template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, class Ld, class St>
+__global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R))
+ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
+    using S = NttShape<LOG_T, LOG_R>;
+    constexpr int T = S::T, R = S::R, NG = S::NG;
+    constexpr int TPS = T / R;  // threads per sub-transform
+    constexpr int SROW = IS_COL ? (COLS + 1) : (T + T / 16);
+    __shared__ u64 sm[IS_COL ? T * (COLS + 1) : COLS * (T + T / 16)];
+
+    const int li = blockIdx.y;
+    const int z = blockIdx.z;
+    const int prime = map.prime[li];
+    const u64 q = tb.q[prime];
+    const u64 q2 = 2 * q;
+    const int n = 1 << a.log_n;
+    const int s2 = a.log_n - LOG_T;  // used by column passes
+    const u64* W = (INV ? tb.itw : tb.tw) + (size_t)prime * n;
+    const u64* Wsh = (INV ? tb.itw_sh : tb.tw_sh) + (size_t)prime * n;
+
+    const int tid = threadIdx.x;
+    int cc, s;
+    if (IS_COL) { cc = tid % COLS; s = tid / COLS; }
+    else { s = tid % TPS; cc = tid / TPS; }
+    const int sub = blockIdx.x * COLS + cc;  // global column / block index
+    const int sub_id = IS_COL ? 0 : sub;
+
+    auto goff = [&](int k) -> int {
+        return IS_COL ? (sub + (k << s2)) : ((sub << LOG_T) + k);
+    };
+    auto sidx = [&](int k) -> int {
+        return IS_COL ? (k * SROW + cc) : (cc * SROW + k + (k >> 4));
+    };
+
+    u64 x[R];
+#pragma unroll
+    for (int g = 0; g < NG; g++) {
+        int lo;
+        if (!INV) {
+            const int hi = LOG_T - g * LOG_R;
+            lo = hi - LOG_R > 0 ? hi - LOG_R : 0;
+        } else {
+            lo = g * LOG_R < LOG_T - LOG_R ? g * LOG_R : LOG_T - LOG_R;
+        }
+        const int base = spread_index(s, lo, LOG_R);
+        if (g == 0) {
+#pragma unroll
+            for (int i = 0; i < R; i++) x[i] = ld(z, li, prime, goff(base + (i << lo)));
+        } else {
+#pragma unroll
+            for (int i = 0; i < R; i++) x[i] = sm[sidx(base + (i << lo))];
+            if (NG > 2) __syncthreads();
+        }
+        if (!INV) {
+            const int qhi = LOG_T - g * LOG_R - 1;
+            const int qlo = qhi - LOG_R + 1 > 0 ? qhi - LOG_R + 1 : 0;
+#pragma unroll
+            for (int qb = qhi; qb >= qlo; qb--) {
+                const int ls = LOG_T - 1 - qb;
+                const int half = 1 << (qb - lo);
+#pragma unroll
+                for (int i = 0; i < R; i++) {
+                    if (i & half) continue;
+                    const int k = base + (i << lo);
+                    const int widx = (((1 << a.st0) + sub_id) << ls) + (k >> (qb + 1));
+                    const u64 w = __ldg(W + widx), wsh = __ldg(Wsh + widx);
+                    u64 u = x[i];
+                    u = u >= q2 ? u - q2 : u;
+                    const u64 t = shoup_lazy(x[i + half], w, wsh, q);
+                    x[i] = u + t;
+                    x[i + half] = u + q2 - t;
+                }
+            }
+        } else {
+            const int qlo = g * LOG_R;
+            const int qhi = (g + 1) * LOG_R < LOG_T ? (g + 1) * LOG_R - 1 : LOG_T - 1;
+            const bool last_stage_pass = (a.st0 == 0);
+#pragma unroll
+            for (int qb = qlo; qb <= qhi; qb++) {
+                const int ls = LOG_T - 1 - qb;
+                const int half = 1 << (qb - lo);
+                const bool fold_ninv = last_stage_pass && ls == 0;
+#pragma unroll
+                for (int i = 0; i < R; i++) {
+                    if (i & half) continue;
+                    const int k = base + (i << lo);
+                    const u64 u = x[i], v = x[i + half];
+                    const u64 t = u + q2 - v;  // (0, 4q)
+                    if (fold_ninv) {
+                        x[i] = shoup_lazy(u + v, tb.ninv[prime], tb.ninv_sh[prime], q);
+                        x[i + half] = shoup_lazy(t, tb.itw1n[prime], tb.itw1n_sh[prime], q);
+                    } else {
+                        const int widx = (((1 << a.st0) + sub_id) << ls) + (k >> (qb + 1));
+                        const u64 w = __ldg(W + widx), wsh = __ldg(Wsh + widx);
+                        u64 sum = u + v;
+                        x[i] = sum >= q2 ? sum - q2 : sum;
+                        x[i + half] = shoup_lazy(t, w, wsh, q);
+                    }
+                }
+            }
+        }
+        if (g == NG - 1) {
+#pragma unroll
+            for (int i = 0; i < R; i++) {
+                u64 v = x[i];
+                if (a.final_out) {
+                    if (!INV) v = v >= q2 ? v - q2 : v;
+                    v = v >= q ? v - q : v;
+                }
+                st(z, li, prime, goff(base + (i << lo)), v);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = x[i];
+            __syncthreads();
+        }
+    }
+}
+
+// ---- plain functors: strided limb buffers -------------------------------
+struct LdBuf {
+    const u64* base;
+    long long item_stride;
+    LimbMap map;  // copy of the offsets (small)
+    int n;
+    __device__ __forceinline__ u64 operator()(int z, int li, int, int off) const {
+        return base[(size_t)z * item_stride + (size_t)map.off[li] * n + off];
+    }
+};
+struct StBuf {
+    u64* base;
+    long long item_stride;
+    LimbMap map;
+    int n;
+    __device__ __forceinline__ void operator()(int z, int li, int, int off, u64 v) const {
+        base[(size_t)z * item_stride + (size_t)map.off[li] * n + off] = v;
+    }
+};
+
+// ---- host-side dispatch ----------------------------------------------------
+// Launch one NTT (forward or inverse) over `count` items x map.count limbs.
+// The first pass reads through `ld`, the last pass writes through `st`; with
+// two passes the intermediate goes through `mid` (item stride mid_stride,
+// limb offsets from map) which may alias the storer's buffer.
+template <int LOG_T, bool IS_COL, bool INV, class Ld, class St>
+static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
+                            int log_n, int st0, int final_out, int count, cudaStream_t s) {
+    constexpr int LOG_R = LOG_T < 4 ? LOG_T : 4;
+    constexpr int T = 1 << LOG_T;
+    // column passes: 16 adjacent columns (128-byte rows); row passes: ~4096 elements per CTA
+    constexpr int COLS_ROW = (4096 / T) > 0 ? (4096 / T) : 1;
+    constexpr int COLS = IS_COL ? 16 : COLS_ROW;
+    const int subs = IS_COL ? (1 << (log_n - LOG_T)) : (1 << (log_n - LOG_T));
+    const int cols = subs < COLS ? subs : COLS;  // tiny rings: fewer sub-transforms than COLS
+    NttPassArgs a{log_n, st0, final_out};
+    dim3 grid(subs / cols, map.count, count);
+    const int threads = T * cols / (1 << LOG_R);
+    if (cols == COLS) {
+        ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV><<<grid, threads, 0, s>>>(ld, st, tb, map, a);
+    } else {
+        // only reachable for single-pass rings (subs == 1)
+        ntt_pass<LOG_T, LOG_R, 1, IS_COL, INV><<<grid, T / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
+    }
+}
+
+template <bool INV, class Ld, class St>
+static void ntt_single(int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
+                       int count, cudaStream_t s) {
+    switch (log_n) {
+#define HELR_SP(LT) case LT: ntt_pass_launch<LT, false, INV>(ld, st, tb, map, log_n, 0, 1, count, s); break;
+        HELR_SP(2) HELR_SP(3) HELR_SP(4) HELR_SP(5) HELR_SP(6) HELR_SP(7) HELR_SP(8) HELR_SP(9)
+        HELR_SP(10) HELR_SP(11)
+#undef HELR_SP
+        default: break;
+    }
+}
+
+template <bool INV, class Ld, class St>
+static void ntt_col(int lt, int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
+                    int final_out, int count, cudaStream_t s) {
+    switch (lt) {
+#define HELR_CP(LT) case LT: ntt_pass_launch<LT, true, INV>(ld, st, tb, map, log_n, 0, final_out, count, s); break;
+        HELR_CP(6) HELR_CP(7) HELR_CP(8)
+#undef HELR_CP
+        default: break;
+    }
+}
+
+template <bool INV, class Ld, class St>
+static void ntt_row(int lt, int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
+                    int final_out, int count, cudaStream_t s) {
+    const int st0 = log_n - lt;
+    switch (lt) {
+#define HELR_RP(LT) case LT: ntt_pass_launch<LT, false, INV>(ld, st, tb, map, log_n, st0, final_out, count, s); break;
+        HELR_RP(6) HELR_RP(7) HELR_RP(8) HELR_RP(9)
+#undef HELR_RP
+        default: break;
+    }
+}
+
+inline int ntt_split_s1(int log_n) { return log_n / 2; }
+
+template <bool INV, class Ld, class St>
+static void ntt_launch(const helr_ctx* c, const Ld& ld, const St& st, u64* mid, long long mid_stride,
+                       const LimbMap& map, int count, cudaStream_t s) {
+    const int log_n = c->log_n;
+    if (log_n <= 11) {
+        ntt_single<INV>(log_n, ld, st, c->t, map, count, s);
+        return;
+    }
+    const int s1 = ntt_split_s1(log_n), s2 = log_n - s1;
+    StBuf smid{mid, mid_stride, map, c->n};
+    LdBuf lmid{mid, mid_stride, map, c->n};
+    if (!INV) {
+        ntt_col<false>(s1, log_n, ld, smid, c->t, map, 0, count, s);
+        ntt_row<false>(s2, log_n, lmid, st, c->t, map, 1, count, s);
+    } else {
+        ntt_row<true>(s2, log_n, ld, smid, c->t, map, 0, count, s);
+        ntt_col<true>(s1, log_n, lmid, st, c->t, map, 1, count, s);
+    }
+}
+
+// Plain buffer-to-buffer NTT (in-place when in == out).
+template <bool INV>
+static void ntt_buffers(const helr_ctx* c, const u64* in, long long in_stride, u64* out, long long out_stride,
+                        const LimbMap& map, int count, cudaStream_t s) {
+    LdBuf ld{in, in_stride, map, c->n};
+    StBuf st{out, out_stride, map, c->n};
+    ntt_launch<INV>(c, ld, st, out, out_stride, map, count, s);
+}

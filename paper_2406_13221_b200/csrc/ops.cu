@@ -1,0 +1,729 @@
+// ops.cu — evaluator operations behind the C ABI (include/helr_ckks.h).
+//
+// Reference mapping (pkg/src/helr/hesim.py): enc 146-158 -> helr_encrypt,
+// dec 160-162 -> helr_decrypt, add 166-175 -> helr_add, cadd 177-184 ->
+// helr_add_const / helr_add_plain, mul 186-195 -> helr_mul_relin +
+// helr_rescale, cmul 197-206 -> helr_mul_const / helr_mul_plain +
+// helr_rescale, imul 208-216 -> helr_imul, rotate 218-226 -> helr_rotate,
+// bootstrap 228-236 -> helr_refresh (stand-in).
+//
+// Key switching (used by mul and rotate) is the hybrid scheme: INTT of the
+// input, per-digit fast basis conversion to the extended basis Q_l + P
+// (ModUp), NTT, inner product with the key, ModDown by P.  All `count`
+// ciphertexts of a call go through every stage together so each key limb is
+// read once per call (key batching across the row blocks of a mini-batch).
+#include <cstdio>
+
+#include "../../include/helr_ckks.h"
+#include "ntt.cuh"
+
+#define CHECK_LAUNCH(what)                                              \
+    do {                                                                \
+        if (!cuda_ok(cudaGetLastError(), what)) return HELR_ECUDA;      \
+    } while (0)
+
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+static inline int blocks_for(long long n, int t) { return (int)((n + t - 1) / t); }
+
+__device__ __forceinline__ int brv_dev(int x, int log_n) { return (int)(__brev((unsigned)x) >> (32 - log_n)); }
+// NTT-slot permutation of X -> X^g: out[i] = in[perm(i)]
+__device__ __forceinline__ int galois_perm(int i, u64 g, int log_n) {
+    const u64 two_n = 2ull << log_n;
+    const u64 e = 2ull * (u64)brv_dev(i, log_n) + 1ull;
+    const u64 f = (e * g) & (two_n - 1);
+    return brv_dev((int)((f - 1) >> 1), log_n);
+}
+
+// ---------------------------------------------------------------------------
+// elementwise kernels.  Items are ciphertexts (2 polys) unless noted; index
+// space: (item, poly, limb, n) flattened with limbs 0..level.
+struct EwGeom {
+    int n, log_n, L, nl;  // nl = level+1 active limbs
+    long long item_stride;  // words between ciphertexts
+};
+__device__ __forceinline__ void ew_decode(long long idx, const EwGeom& g, int& item, int& poly, int& limb, int& k) {
+    k = (int)(idx & (g.n - 1));
+    long long r = idx >> g.log_n;
+    limb = (int)(r % g.nl);
+    r /= g.nl;
+    poly = (int)(r & 1);
+    item = (int)(r >> 1);
+}
+__device__ __forceinline__ size_t ew_off(const EwGeom& g, int item, int poly, int limb, int k) {
+    return (size_t)item * g.item_stride + ((size_t)poly * g.L + limb) * g.n + k;
+}
+
+enum EwOp { EW_ADD = 0, EW_SUB, EW_ADDC, EW_ADDPT, EW_MULC, EW_MULPT, EW_IMUL };
+
+__global__ void k_elementwise(int op, const u64* a, const u64* b, u64* out, EwGeom g, long long total,
+                              Tables tb, const u64* imul_f) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        int item, poly, limb, k;
+        ew_decode(idx, g, item, poly, limb, k);
+        const u64 q = tb.q[limb];
+        const size_t o = ew_off(g, item, poly, limb, k);
+        const u64 x = a[o];
+        u64 r;
+        switch (op) {
+            case EW_ADD: r = add_mod(x, b[o], q); break;
+            case EW_SUB: r = sub_mod(x, b[o], q); break;
+            case EW_ADDC: r = poly == 0 ? add_mod(x, b[limb], q) : x; break;
+            case EW_ADDPT: r = poly == 0 ? add_mod(x, b[(size_t)limb * g.n + k], q) : x; break;
+            case EW_MULC: r = mul_mod(x, b[limb], q, tb.br1[limb], tb.br0[limb]); break;
+            case EW_MULPT: r = mul_mod(x, b[(size_t)limb * g.n + k], q, tb.br1[limb], tb.br0[limb]); break;
+            default: r = mul_mod(x, imul_f[(size_t)limb * g.n + k], q, tb.br1[limb], tb.br0[limb]); break;
+        }
+        out[o] = r;
+    }
+}
+
+static int launch_ew(helr_ctx* c, int op, const u64* a, const u64* b, u64* out, int count, int level, void* s) {
+    if (level < 0 || level >= c->L || count < 0) { set_error("bad level/count"); return HELR_EINVAL; }
+    if (count == 0) return HELR_OK;
+    EwGeom g{c->n, c->log_n, c->L, level + 1, 2ll * c->L * c->n};
+    long long total = (long long)count * 2 * (level + 1) * c->n;
+    int blocks = blocks_for(total, 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_elementwise<<<blocks, 256, 0, S(s)>>>(op, a, b, out, g, total, c->t, c->imul_f);
+    CHECK_LAUNCH("elementwise");
+    return HELR_OK;
+}
+
+extern "C" int helr_add(helr_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, int count, int level, void* s) {
+    return launch_ew(c, EW_ADD, (const u64*)a, (const u64*)b, (u64*)out, count, level, s);
+}
+extern "C" int helr_sub(helr_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, int count, int level, void* s) {
+    return launch_ew(c, EW_SUB, (const u64*)a, (const u64*)b, (u64*)out, count, level, s);
+}
+extern "C" int helr_add_const(helr_ctx* c, const uint64_t* a, const uint64_t* k, uint64_t* out, int count, int level, void* s) {
+    return launch_ew(c, EW_ADDC, (const u64*)a, (const u64*)k, (u64*)out, count, level, s);
+}
+extern "C" int helr_add_plain(helr_ctx* c, const uint64_t* a, const uint64_t* pt, uint64_t* out, int count, int level, void* s) {
+    return launch_ew(c, EW_ADDPT, (const u64*)a, (const u64*)pt, (u64*)out, count, level, s);
+}
+extern "C" int helr_mul_const(helr_ctx* c, const uint64_t* a, const uint64_t* k, uint64_t* out, int count, int level, void* s) {
+    return launch_ew(c, EW_MULC, (const u64*)a, (const u64*)k, (u64*)out, count, level, s);
+}
+extern "C" int helr_mul_plain(helr_ctx* c, const uint64_t* a, const uint64_t* pt, uint64_t* out, int count, int level, void* s) {
+    return launch_ew(c, EW_MULPT, (const u64*)a, (const u64*)pt, (u64*)out, count, level, s);
+}
+extern "C" int helr_imul(helr_ctx* c, const uint64_t* a, uint64_t* out, int count, int level, void* s) {
+    return launch_ew(c, EW_IMUL, (const u64*)a, nullptr, (u64*)out, count, level, s);
+}
+
+// ---------------------------------------------------------------------------
+// NTT entry points
+extern "C" int helr_ntt_fwd(helr_ctx* c, uint64_t* data, int first_prime, int n_limbs, int count, int64_t stride,
+                            void* s) {
+    if (first_prime < 0 || n_limbs < 1 || first_prime + n_limbs > c->LK) { set_error("bad limb range"); return HELR_EINVAL; }
+    if (count < 1) return HELR_OK;
+    LimbMap m = limb_range(first_prime, n_limbs);
+    ntt_buffers<false>(c, (const u64*)data, stride, (u64*)data, stride, m, count, S(s));
+    CHECK_LAUNCH("ntt_fwd");
+    return HELR_OK;
+}
+extern "C" int helr_ntt_inv(helr_ctx* c, uint64_t* data, int first_prime, int n_limbs, int count, int64_t stride,
+                            void* s) {
+    if (first_prime < 0 || n_limbs < 1 || first_prime + n_limbs > c->LK) { set_error("bad limb range"); return HELR_EINVAL; }
+    if (count < 1) return HELR_OK;
+    LimbMap m = limb_range(first_prime, n_limbs);
+    ntt_buffers<true>(c, (const u64*)data, stride, (u64*)data, stride, m, count, S(s));
+    CHECK_LAUNCH("ntt_inv");
+    return HELR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// keys
+__global__ void k_fill_secret(u64* sk, int n, int LK, u64 seed, Tables tb) {
+    const u64 key = prng_key(seed, stream_id(ST_SK, 0, 0, PU_S));
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const long long sv = (long long)(prng_at(key, (u64)i) % 3ull) - 1;
+        for (int p = 0; p < LK; p++) sk[(size_t)p * n + i] = reduce_i64(sv, tb.q[p]);
+    }
+}
+
+extern "C" int helr_keygen_secret(helr_ctx* c, uint64_t* sk, uint64_t seed, void* s) {
+    k_fill_secret<<<blocks_for(c->n, 256), 256, 0, S(s)>>>((u64*)sk, c->n, c->LK, seed, c->t);
+    CHECK_LAUNCH("keygen_secret");
+    LimbMap m = limb_range(0, c->LK);
+    ntt_buffers<false>(c, (const u64*)sk, 0, (u64*)sk, 0, m, 1, S(s));
+    CHECK_LAUNCH("keygen_secret ntt");
+    return HELR_OK;
+}
+
+// evk[j][0][p] := e_j mod q_p  (coefficient form; NTT'd afterwards)
+__global__ void k_fill_key_error(u64* evk, int n, int LK, int beta, u64 seed, u64 key_id, int eta, Tables tb) {
+    const int j = blockIdx.y;
+    const u64 key = prng_key(seed, stream_id(ST_KEY, key_id, (u64)j, PU_E));
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const long long e = cbd_from(prng_at(key, (u64)i), eta);
+        for (int p = 0; p < LK; p++) evk[(((size_t)j * 2) * LK + p) * n + i] = reduce_i64(e, tb.q[p]);
+    }
+}
+// b1 = a (uniform), b0 = e - a*s + [p in digit j] * (P mod q_p) * s'
+__global__ void k_key_combine(u64* evk, const u64* sk, int n, int log_n, int L, int LK, int alpha, u64 seed,
+                              u64 key_id, long long galois, Tables tb, const u64* pmod) {
+    const int j = blockIdx.z, p = blockIdx.y;
+    const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
+    const u64 key = prng_key(seed, stream_id(ST_KEY, key_id, (u64)j, PU_A));
+    const bool in_digit = p < L && p / alpha == j;
+    const u64 f = in_digit ? pmod[p] : 0;
+    const u64* sp = sk + (size_t)p * n;
+    u64* b0 = evk + (((size_t)j * 2) * LK + p) * n;
+    u64* b1 = evk + (((size_t)j * 2 + 1) * LK + p) * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const u64 ctr = 2ull * ((u64)p * n + i);
+        const u64 a = uniform_from(prng_at(key, ctr), prng_at(key, ctr + 1), q, r1, r0);
+        u64 v = sub_mod(b0[i], mul_mod(a, sp[i], q, r1, r0), q);
+        if (in_digit) {
+            u64 s2;
+            if (galois == 0) s2 = mul_mod(sp[i], sp[i], q, r1, r0);
+            else s2 = sp[galois_perm(i, (u64)galois, log_n)];
+            v = add_mod(v, mul_mod(f, s2, q, r1, r0), q);
+        }
+        b0[i] = v;
+        b1[i] = a;
+    }
+}
+
+extern "C" int helr_keygen_switch(helr_ctx* c, const uint64_t* sk, int64_t galois, uint64_t* evk, uint64_t seed,
+                                  uint64_t key_id, void* s) {
+    if (galois != 0 && ((galois & 1) == 0 || galois < 0)) { set_error("galois element must be odd and positive"); return HELR_EINVAL; }
+    galois = galois % (2ll * c->n);
+    dim3 g1(blocks_for(c->n, 256), c->beta);
+    k_fill_key_error<<<g1, 256, 0, S(s)>>>((u64*)evk, c->n, c->LK, c->beta, seed, key_id, c->eta, c->t);
+    CHECK_LAUNCH("keygen error");
+    LimbMap m = limb_range(0, c->LK);
+    const long long st = 2ll * c->LK * c->n;
+    ntt_buffers<false>(c, (const u64*)evk, st, (u64*)evk, st, m, c->beta, S(s));
+    CHECK_LAUNCH("keygen ntt");
+    dim3 g2(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, c->LK, c->beta);
+    k_key_combine<<<g2, 256, 0, S(s)>>>((u64*)evk, (const u64*)sk, c->n, c->log_n, c->L, c->LK, c->alpha, seed, key_id,
+                                        (long long)galois, c->t, c->pmod);
+    CHECK_LAUNCH("keygen combine");
+    return HELR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// encryption / decryption
+__global__ void k_enc_fill(u64* ct, const long long* msg, int n, int L, int nl, u64 seed, u64 first_id, int eta,
+                           Tables tb) {
+    const int b = blockIdx.y;
+    const u64 key = prng_key(seed, stream_id(ST_CT, first_id + (u64)b, 0, PU_E));
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const long long v = msg[(size_t)b * n + i] + cbd_from(prng_at(key, (u64)i), eta);
+        for (int p = 0; p < nl; p++) ct[(size_t)b * 2 * L * n + (size_t)p * n + i] = reduce_i64(v, tb.q[p]);
+    }
+}
+__global__ void k_enc_combine(u64* ct, const u64* sk, int n, int L, u64 seed, u64 first_id, Tables tb) {
+    const int b = blockIdx.z, p = blockIdx.y;
+    const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
+    const u64 key = prng_key(seed, stream_id(ST_CT, first_id + (u64)b, 0, PU_A));
+    u64* c0 = ct + (size_t)b * 2 * L * n + (size_t)p * n;
+    u64* c1 = c0 + (size_t)L * n;
+    const u64* sp = sk + (size_t)p * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const u64 ctr = 2ull * ((u64)p * n + i);
+        const u64 a = uniform_from(prng_at(key, ctr), prng_at(key, ctr + 1), q, r1, r0);
+        c1[i] = a;
+        c0[i] = sub_mod(c0[i], mul_mod(a, sp[i], q, r1, r0), q);
+    }
+}
+
+static int encrypt_dev(helr_ctx* c, const u64* sk, const long long* msg, u64* ct, int count, int level, u64 seed,
+                       u64 first_id, cudaStream_t s) {
+    dim3 g1(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
+    k_enc_fill<<<g1, 256, 0, s>>>(ct, msg, c->n, c->L, level + 1, seed, first_id, c->eta, c->t);
+    CHECK_LAUNCH("encrypt fill");
+    LimbMap m = limb_range(0, level + 1);
+    const long long st = 2ll * c->L * c->n;
+    ntt_buffers<false>(c, ct, st, ct, st, m, count, s);
+    CHECK_LAUNCH("encrypt ntt");
+    dim3 g2(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, count);
+    k_enc_combine<<<g2, 256, 0, s>>>(ct, sk, c->n, c->L, seed, first_id, c->t);
+    CHECK_LAUNCH("encrypt combine");
+    return HELR_OK;
+}
+
+extern "C" int helr_encrypt(helr_ctx* c, const uint64_t* sk, const int64_t* msg, uint64_t* ct, int count, int level,
+                            uint64_t seed, uint64_t first_id, void* s) {
+    if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    if (count < 1) return HELR_OK;
+    return encrypt_dev(c, (const u64*)sk, (const long long*)msg, (u64*)ct, count, level, seed, first_id, S(s));
+}
+
+__global__ void k_dec_combine(const u64* ct, const u64* sk, u64* v, int n, int L, Tables tb) {
+    const int b = blockIdx.y;
+    const u64 q = tb.q[0], r1 = tb.br1[0], r0 = tb.br0[0];
+    const u64* c0 = ct + (size_t)b * 2 * L * n;
+    const u64* c1 = c0 + (size_t)L * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        v[(size_t)b * n + i] = add_mod(c0[i], mul_mod(c1[i], sk[i], q, r1, r0), q);
+}
+__global__ void k_center(const u64* v, long long* out, long long total, double ratio, Tables tb) {
+    const u64 q = tb.q[0];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const u64 x = v[i];
+        long long m = x > (q >> 1) ? (long long)x - (long long)q : (long long)x;
+        if (ratio != 1.0) m = __double2ll_rn(__dmul_rn(__ll2double_rn(m), ratio));
+        out[i] = m;
+    }
+}
+
+static int decrypt_dev(helr_ctx* c, const u64* sk, const u64* ct, int count, long long* out, double ratio,
+                       u64* tmp, cudaStream_t s) {
+    dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
+    k_dec_combine<<<g, 256, 0, s>>>(ct, sk, tmp, c->n, c->L, c->t);
+    CHECK_LAUNCH("decrypt combine");
+    LimbMap m = limb_range(0, 1);
+    ntt_buffers<true>(c, tmp, c->n, tmp, c->n, m, count, s);
+    CHECK_LAUNCH("decrypt intt");
+    long long total = (long long)count * c->n;
+    k_center<<<blocks_for(total, 256) < 4096 ? blocks_for(total, 256) : 4096, 256, 0, s>>>(tmp, out, total, ratio, c->t);
+    CHECK_LAUNCH("decrypt center");
+    return HELR_OK;
+}
+
+extern "C" int helr_decrypt(helr_ctx* c, const uint64_t* sk, const uint64_t* ct, int count, int level, int64_t* out,
+                            void* s) {
+    if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    for (int b0 = 0; b0 < count; b0 += c->max_batch) {
+        int nb = count - b0 < c->max_batch ? count - b0 : c->max_batch;
+        int r = decrypt_dev(c, (const u64*)sk, (const u64*)ct + (size_t)b0 * 2 * c->L * c->n, nb,
+                            (long long*)out + (size_t)b0 * c->n, 1.0, c->ws, S(s));
+        if (r) return r;
+    }
+    return HELR_OK;
+}
+
+__global__ void k_plain_fill(const long long* msg, u64* pt, int n, int L, int nl, Tables tb) {
+    const int b = blockIdx.y;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const long long v = msg[(size_t)b * n + i];
+        for (int p = 0; p < nl; p++) pt[((size_t)b * L + p) * n + i] = reduce_i64(v, tb.q[p]);
+    }
+}
+extern "C" int helr_encode_plain(helr_ctx* c, const int64_t* msg, uint64_t* pt, int count, int level, void* s) {
+    if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    if (count < 1) return HELR_OK;
+    dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
+    k_plain_fill<<<g, 256, 0, S(s)>>>((const long long*)msg, (u64*)pt, c->n, c->L, level + 1, c->t);
+    CHECK_LAUNCH("plain fill");
+    LimbMap m = limb_range(0, level + 1);
+    const long long st = (long long)c->L * c->n;
+    ntt_buffers<false>(c, (const u64*)pt, st, (u64*)pt, st, m, count, S(s));
+    CHECK_LAUNCH("plain ntt");
+    return HELR_OK;
+}
+
+extern "C" int helr_refresh(helr_ctx* c, const uint64_t* sk, const uint64_t* a, int in_level, double ratio,
+                            uint64_t* out, int out_level, int count, uint64_t seed, uint64_t first_id, void* s) {
+    if (in_level < 0 || in_level >= c->L || out_level < 0 || out_level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    // workspace: [B][N] u64 scratch + [B][N] int64 message
+    const int chunk = c->max_batch;
+    for (int b0 = 0; b0 < count; b0 += chunk) {
+        int nb = count - b0 < chunk ? count - b0 : chunk;
+        u64* tmp = c->ws;
+        long long* msg = (long long*)(c->ws + (size_t)chunk * c->n);
+        int r = decrypt_dev(c, (const u64*)sk, (const u64*)a + (size_t)b0 * 2 * c->L * c->n, nb, msg, ratio, tmp, S(s));
+        if (r) return r;
+        r = encrypt_dev(c, (const u64*)sk, msg, (u64*)out + (size_t)b0 * 2 * c->L * c->n, nb, out_level, seed,
+                        first_id + (u64)b0, S(s));
+        if (r) return r;
+    }
+    return HELR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// rescale: out_i = (x_i - NTT_i([INTT_l(x_l)]_centred mod q_i)) * q_l^-1
+__global__ void k_rescale_conv(const u64* r, u64* t, int n, int l, Tables tb) {
+    // r: [items][N] coefficient form mod q_l;  t: [items][l][N]
+    const int it = blockIdx.y;
+    const u64 ql = tb.q[l], half = ql >> 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const u64 v = r[(size_t)it * n + i];
+        for (int p = 0; p < l; p++) {
+            const u64 q = tb.q[p];
+            u64 w = v > half ? neg_mod((ql - v) % q, q) : v % q;
+            t[((size_t)it * l + p) * n + i] = w;
+        }
+    }
+}
+__global__ void k_rescale_final(const u64* x, const u64* t, u64* out, int n, int L, int l, const u64* qlinv,
+                                const u64* qlinv_sh, Tables tb) {
+    const int it = blockIdx.z, p = blockIdx.y;  // it = item*2 + poly
+    const u64 q = tb.q[p];
+    const u64 w = qlinv[(size_t)l * L + p], wsh = qlinv_sh[(size_t)l * L + p];
+    const u64* xp = x + ((size_t)it * L + p) * n;
+    const u64* tp = t + ((size_t)it * l + p) * n;
+    u64* op = out + ((size_t)it * L + p) * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        op[i] = shoup(sub_mod(xp[i], tp[i], q), w, wsh, q);
+}
+
+static int rescale_dev(helr_ctx* c, const u64* a, u64* out, int count, int level, cudaStream_t s) {
+    const int n = c->n, L = c->L, l = level;
+    const int items = 2 * count;  // polynomials
+    u64* r = c->ws;                                // [items][N]
+    u64* t = c->ws + (size_t)items * n;            // [items][l][N]
+    // r = INTT(limb l) per polynomial (polynomial stride L*N)
+    {
+        LimbMap m; m.count = 1; m.off[0] = 0; m.prime[0] = (unsigned char)l;
+        LdBuf ld{a + (size_t)l * n, (long long)L * n, m, n};
+        StBuf st{r, (long long)n, m, n};
+        ntt_launch<true>(c, ld, st, r, n, m, items, s);
+        CHECK_LAUNCH("rescale intt");
+    }
+    dim3 g1(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, items);
+    k_rescale_conv<<<g1, 256, 0, s>>>(r, t, n, l, c->t);
+    CHECK_LAUNCH("rescale conv");
+    LimbMap m = limb_range(0, l);
+    ntt_buffers<false>(c, t, (long long)l * n, t, (long long)l * n, m, items, s);
+    CHECK_LAUNCH("rescale ntt");
+    dim3 g2(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, l, items);
+    k_rescale_final<<<g2, 256, 0, s>>>(a, t, out, n, L, l, c->qlinv, c->qlinv_sh, c->t);
+    CHECK_LAUNCH("rescale final");
+    return HELR_OK;
+}
+
+extern "C" int helr_rescale(helr_ctx* c, const uint64_t* a, uint64_t* out, int count, int level, void* s) {
+    if (level < 1 || level >= c->L) { set_error("rescale needs level >= 1"); return HELR_EINVAL; }
+    const size_t need = (size_t)2 * (level + 1) * c->n;  // per ciphertext (r + t)
+    int chunk = (int)(c->ws_words / need);
+    if (chunk < 1) { set_error("workspace too small"); return HELR_ENOMEM; }
+    for (int b0 = 0; b0 < count; b0 += chunk) {
+        int nb = count - b0 < chunk ? count - b0 : chunk;
+        size_t off = (size_t)b0 * 2 * c->L * c->n;
+        int r = rescale_dev(c, (const u64*)a + off, (u64*)out + off, nb, level, S(s));
+        if (r) return r;
+    }
+    return HELR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// key switching
+struct KsInput {
+    const u64* d;        // NTT-form polynomial of item b at d + b*d_stride, limb stride N
+    long long d_stride;
+    long long galois;    // 0: none, else apply X -> X^galois to d first
+};
+struct KsEpilogue {
+    u64* out;             // ciphertext of item b at out + b*out_stride
+    long long out_stride;
+    const u64* add_a;     // optional ciphertext-like addend (both polys), stride add_a_stride
+    long long add_a_stride;
+    const u64* add_p;     // optional: poly 0 of add_p permuted by galois, added to out poly 0
+    long long add_p_stride;
+    long long galois;
+};
+
+// ModUp conversion for digit j; grid (x: coeff tiles, y: digit, z: item)
+struct ModUpArgs {
+    const u64* coef;   // [B][nl][N] INTT of d
+    long long coef_stride;
+    const u64* d;      // NTT-form input (own-digit limbs are copied from here)
+    long long d_stride;
+    long long galois;
+    u64* ext;          // [B][beta][ext][N]
+    long long ext_item_stride, ext_digit_stride;
+    const u64* tab;    // d_tab
+    const size_t* offs;// device array of modup offsets for this level (per digit)
+    int n, log_n, nl, K, L, alpha;
+};
+__global__ void k_modup(ModUpArgs a, Tables tb) {
+    const int j = blockIdx.y, b = blockIdx.z;
+    const int lo = j * a.alpha, hi = lo + a.alpha < a.nl ? lo + a.alpha : a.nl;
+    const int ns = hi - lo;
+    const int ne = a.nl + a.K;
+    const int nt = ne - ns;
+    const u64* T = a.tab + a.offs[j];
+    const u64* hv = T;
+    const u64* hvs = T + ns;
+    const u64* hm = T + 2 * ns;
+    const u64* hms = hm + (size_t)ns * nt;
+    u64* ext = a.ext + (size_t)b * a.ext_item_stride + (size_t)j * a.ext_digit_stride;
+    const u64* coef = a.coef + (size_t)b * a.coef_stride;
+    const u64* d = a.d + (size_t)b * a.d_stride;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+        u64 y[HELR_MAXP];
+        const int src_i = a.galois ? galois_perm(i, (u64)a.galois, a.log_n) : i;
+#pragma unroll 4
+        for (int k = 0; k < ns; k++) {
+            const int p = lo + k;
+            y[k] = shoup(coef[(size_t)p * a.n + i], hv[k], hvs[k], tb.q[p]);
+            ext[(size_t)p * a.n + i] = d[(size_t)p * a.n + src_i];
+        }
+        int t = 0;
+        for (int e = 0; e < ne; e++) {
+            if (e >= lo && e < hi) continue;
+            const int p = e < a.nl ? e : a.L + (e - a.nl);
+            const u64 q = tb.q[p];
+            u64 acc = 0;
+            for (int k = 0; k < ns; k++)
+                acc = add_mod(acc, shoup(y[k], hm[(size_t)k * nt + t], hms[(size_t)k * nt + t], q), q);
+            ext[(size_t)e * a.n + i] = acc;
+            t++;
+        }
+    }
+}
+
+// inner product: acc[b][poly][e] = sum_j ext[b][j][e] * evk[j][poly][prime(e)]
+template <int BT>
+__global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long ext_digit_stride, const u64* evk,
+                           u64* acc, long long acc_item_stride, int n, int nl, int K, int L, int LK, int nd, int B,
+                           Tables tb) {
+    const int e = blockIdx.y;
+    const int p = e < nl ? e : L + (e - nl);
+    const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        for (int b0 = 0; b0 < B; b0 += BT) {
+            u128v a0[BT], a1[BT];
+#pragma unroll
+            for (int x = 0; x < BT; x++) { a0[x] = u128v{0, 0}; a1[x] = u128v{0, 0}; }
+            for (int j = 0; j < nd; j++) {
+                const u64 k0 = evk[(((size_t)j * 2) * LK + p) * n + i];
+                const u64 k1 = evk[(((size_t)j * 2 + 1) * LK + p) * n + i];
+#pragma unroll
+                for (int x = 0; x < BT; x++) {
+                    if (b0 + x < B) {
+                        const u64 u = ext[(size_t)(b0 + x) * ext_item_stride + (size_t)j * ext_digit_stride +
+                                          (size_t)e * n + i];
+                        acc_wide(a0[x], u, k0);
+                        acc_wide(a1[x], u, k1);
+                    }
+                }
+                if ((j & 3) == 3 && j + 1 < nd) {
+#pragma unroll
+                    for (int x = 0; x < BT; x++) {
+                        a0[x] = u128v{0, barrett128(a0[x], q, r1, r0)};
+                        a1[x] = u128v{0, barrett128(a1[x], q, r1, r0)};
+                    }
+                }
+            }
+#pragma unroll
+            for (int x = 0; x < BT; x++) {
+                if (b0 + x < B) {
+                    u64* ap = acc + (size_t)(b0 + x) * acc_item_stride;
+                    ap[(size_t)e * n + i] = barrett128(a0[x], q, r1, r0);
+                    ap[((size_t)(nl + K) + e) * n + i] = barrett128(a1[x], q, r1, r0);
+                }
+            }
+        }
+    }
+}
+
+// ModDown conversion: mdc[b][poly][i] = sum_k [a_k * phinv_k]_{p_k} * phmod[k][i] mod q_i
+__global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n,
+                               int nl, int K, int L, const u64* phinv, const u64* phinv_sh, const u64* phm,
+                               const u64* phms, Tables tb) {
+    const int it = blockIdx.y;  // item*2 + poly
+    const int b = it >> 1, poly = it & 1;
+    const int ne = nl + K;
+    const u64* ap = acc + (size_t)b * acc_item_stride + (size_t)poly * ne * n;
+    u64* mp = mdc + (size_t)b * mdc_item_stride + (size_t)poly * L * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        u64 z[HELR_MAXP];
+        for (int k = 0; k < K; k++) {
+            const u64 pk = tb.q[L + k];
+            z[k] = shoup(ap[(size_t)(nl + k) * n + i], phinv[k], phinv_sh[k], pk);
+        }
+        for (int p = 0; p < nl; p++) {
+            const u64 q = tb.q[p];
+            u64 s = 0;
+            for (int k = 0; k < K; k++)
+                s = add_mod(s, shoup(z[k], phm[(size_t)k * L + p], phms[(size_t)k * L + p], q), q);
+            mp[(size_t)p * n + i] = s;
+        }
+    }
+}
+
+__global__ void k_moddown_final(const u64* acc, long long acc_item_stride, const u64* mdc, long long mdc_item_stride,
+                                KsEpilogue ep, int n, int log_n, int nl, int K, int L, const u64* pinv,
+                                const u64* pinv_sh, Tables tb) {
+    const int p = blockIdx.y;
+    const int it = blockIdx.z, b = it >> 1, poly = it & 1;
+    const int ne = nl + K;
+    const u64 q = tb.q[p];
+    const u64* ap = acc + (size_t)b * acc_item_stride + ((size_t)poly * ne + p) * n;
+    const u64* mp = mdc + (size_t)b * mdc_item_stride + ((size_t)poly * L + p) * n;
+    u64* op = ep.out + (size_t)b * ep.out_stride + ((size_t)poly * L + p) * n;
+    const u64* aa = ep.add_a ? ep.add_a + (size_t)b * ep.add_a_stride + ((size_t)poly * L + p) * n : nullptr;
+    const u64* pp = (ep.add_p && poly == 0) ? ep.add_p + (size_t)b * ep.add_p_stride + (size_t)p * n : nullptr;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        u64 v = shoup(sub_mod(ap[i], mp[i], q), pinv[p], pinv_sh[p], q);
+        if (aa) v = add_mod(v, aa[i], q);
+        if (pp) v = add_mod(v, pp[galois_perm(i, (u64)ep.galois, log_n)], q);
+        op[i] = v;
+    }
+}
+
+// Loader applying the Galois permutation to a plain buffer (rotation input).
+struct LdPerm {
+    const u64* base;
+    long long item_stride;
+    int n, log_n;
+    u64 g;
+    __device__ __forceinline__ u64 operator()(int z, int li, int, int off) const {
+        return base[(size_t)z * item_stride + (size_t)li * n + galois_perm(off, g, log_n)];
+    }
+};
+
+// workspace carve-up for key switching of B items at level l
+struct KsWs {
+    u64 *coef, *ext, *acc, *mdc, *tensor;
+    long long coef_s, ext_s, ext_ds, acc_s, mdc_s;
+};
+static KsWs ks_ws(helr_ctx* c, int B) {
+    KsWs w;
+    const size_t n = c->n;
+    w.coef_s = (long long)c->L * n;
+    w.ext_ds = (long long)c->LK * n;
+    w.ext_s = (long long)c->beta * w.ext_ds;
+    w.acc_s = 2ll * c->LK * n;
+    w.mdc_s = 2ll * c->L * n;
+    w.coef = c->ws;
+    w.ext = w.coef + (size_t)B * w.coef_s;
+    w.acc = w.ext + (size_t)B * w.ext_s;
+    w.mdc = w.acc + (size_t)B * w.acc_s;
+    w.tensor = w.mdc + (size_t)B * w.mdc_s;
+    return w;
+}
+
+static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, KsEpilogue ep, int B, const KsWs& w,
+                           cudaStream_t s) {
+    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
+    const int nd = (nl + c->alpha - 1) / c->alpha;
+    // 1) coef = INTT(sigma(d))
+    {
+        LimbMap m = limb_range(0, nl);
+        StBuf st{w.coef, w.coef_s, m, n};
+        if (in.galois) {
+            LdPerm ld{in.d, in.d_stride, n, c->log_n, (u64)in.galois};
+            ntt_launch<true>(c, ld, st, w.coef, w.coef_s, m, B, s);
+        } else {
+            LdBuf ld{in.d, in.d_stride, m, n};
+            ntt_launch<true>(c, ld, st, w.coef, w.coef_s, m, B, s);
+        }
+        CHECK_LAUNCH("ks intt");
+    }
+    // 2) ModUp conversions (+ copy of own-digit NTT limbs)
+    {
+        ModUpArgs a{w.coef, w.coef_s, in.d, in.d_stride, in.galois, w.ext, w.ext_s, w.ext_ds, c->d_tab, c->d_modup_offs + (size_t)level * c->beta,
+                    n, c->log_n, nl, K, L, c->alpha};
+        dim3 g(blocks_for(n, 128) < 64 ? blocks_for(n, 128) : 64, nd, B);
+        k_modup<<<g, 128, 0, s>>>(a, c->t);
+        CHECK_LAUNCH("ks modup");
+    }
+    // 3) NTT of the converted limbs, per digit
+    for (int j = 0; j < nd; j++) {
+        const int lo = j * c->alpha, hi = lo + c->alpha < nl ? lo + c->alpha : nl;
+        LimbMap m;
+        m.count = 0;
+        for (int e = 0; e < ne; e++) {
+            if (e >= lo && e < hi) continue;
+            m.off[m.count] = (unsigned char)e;
+            m.prime[m.count] = (unsigned char)(e < nl ? e : L + (e - nl));
+            m.count++;
+        }
+        u64* base = w.ext + (size_t)j * w.ext_ds;
+        ntt_buffers<false>(c, base, w.ext_s, base, w.ext_s, m, B, s);
+        CHECK_LAUNCH("ks modup ntt");
+    }
+    // 4) inner product with the key
+    {
+        dim3 g(blocks_for(n, 256) < 32 ? blocks_for(n, 256) : 32, ne);
+        k_ks_inner<4><<<g, 256, 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B, c->t);
+        CHECK_LAUNCH("ks inner");
+    }
+    // 5) ModDown: INTT of the P limbs (both polys), conversion, NTT, combine
+    {
+        LimbMap m;
+        m.count = K;
+        for (int k = 0; k < K; k++) { m.off[k] = (unsigned char)(nl + k); m.prime[k] = (unsigned char)(L + k); }
+        // items: (b, poly) with poly stride ne*N inside acc item
+        // run per poly to keep a single item stride
+        for (int poly = 0; poly < 2; poly++) {
+            u64* base = w.acc + (size_t)poly * ne * n;
+            ntt_buffers<true>(c, base, w.acc_s, base, w.acc_s, m, B, s);
+        }
+        CHECK_LAUNCH("ks moddown intt");
+        dim3 g(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, 2 * B);
+        k_moddown_conv<<<g, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv, c->md_phinv_sh,
+                                         c->md_phmod, c->md_phmod_sh, c->t);
+        CHECK_LAUNCH("ks moddown conv");
+        LimbMap mq = limb_range(0, nl);
+        for (int poly = 0; poly < 2; poly++) {
+            u64* base = w.mdc + (size_t)poly * L * n;
+            ntt_buffers<false>(c, base, w.mdc_s, base, w.mdc_s, mq, B, s);
+        }
+        CHECK_LAUNCH("ks moddown ntt");
+        dim3 g2(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, nl, 2 * B);
+        k_moddown_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, ep, n, c->log_n, nl, K, L, c->md_pinv,
+                                           c->md_pinv_sh, c->t);
+        CHECK_LAUNCH("ks moddown final");
+    }
+    return HELR_OK;
+}
+
+// tensor: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1   (into [B][3][L][N])
+__global__ void k_tensor(const u64* a, const u64* b, u64* d, int n, int L, int nl, Tables tb) {
+    const int p = blockIdx.y, it = blockIdx.z;
+    const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
+    const u64* a0 = a + (size_t)it * 2 * L * n + (size_t)p * n;
+    const u64* a1 = a0 + (size_t)L * n;
+    const u64* b0 = b + (size_t)it * 2 * L * n + (size_t)p * n;
+    const u64* b1 = b0 + (size_t)L * n;
+    u64* d0 = d + (size_t)it * 3 * L * n + (size_t)p * n;
+    u64* d1 = d0 + (size_t)L * n;
+    u64* d2 = d1 + (size_t)L * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const u64 x0 = a0[i], x1 = a1[i], y0 = b0[i], y1 = b1[i];
+        d0[i] = mul_mod(x0, y0, q, r1, r0);
+        u128v m = mul_wide(x0, y1);
+        acc_wide(m, x1, y0);
+        d1[i] = barrett128(m, q, r1, r0);
+        d2[i] = mul_mod(x1, y1, q, r1, r0);
+    }
+}
+
+extern "C" int helr_mul_relin(helr_ctx* c, const uint64_t* a, const uint64_t* b, const uint64_t* rlk, uint64_t* out,
+                              int count, int level, void* s) {
+    if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    const int chunk = c->max_batch;
+    const long long cs = 2ll * c->L * c->n;
+    for (int b0 = 0; b0 < count; b0 += chunk) {
+        int nb = count - b0 < chunk ? count - b0 : chunk;
+        KsWs w = ks_ws(c, chunk);
+        dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, nb);
+        k_tensor<<<g, 256, 0, S(s)>>>((const u64*)a + b0 * cs, (const u64*)b + b0 * cs, w.tensor, c->n, c->L, level + 1, c->t);
+        CHECK_LAUNCH("tensor");
+        const long long ts = 3ll * c->L * c->n;
+        KsInput in{w.tensor + 2ll * c->L * c->n, ts, 0};
+        KsEpilogue ep{(u64*)out + b0 * cs, cs, w.tensor, ts, nullptr, 0, 0};
+        int r = keyswitch_batch(c, in, (const u64*)rlk, level, ep, nb, w, S(s));
+        if (r) return r;
+    }
+    return HELR_OK;
+}
+
+extern "C" int helr_rotate(helr_ctx* c, const uint64_t* a, int64_t galois, const uint64_t* gk, uint64_t* out, int count,
+                           int level, int accumulate, void* s) {
+    if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    if (galois <= 0 || (galois & 1) == 0) { set_error("galois element must be odd and positive"); return HELR_EINVAL; }
+    if (a == out) { set_error("helr_rotate: out must not alias the input"); return HELR_EINVAL; }
+    const int chunk = c->max_batch;
+    const long long cs = 2ll * c->L * c->n;
+    const long long g = (long long)(galois % (2ll * c->n));
+    for (int b0 = 0; b0 < count; b0 += chunk) {
+        int nb = count - b0 < chunk ? count - b0 : chunk;
+        KsWs w = ks_ws(c, chunk);
+        const u64* ab = (const u64*)a + b0 * cs;
+        KsInput in{ab + (size_t)c->L * c->n, cs, g};
+        KsEpilogue ep{(u64*)out + b0 * cs, cs, accumulate ? ab : nullptr, cs, ab, cs, g};
+        int r = keyswitch_batch(c, in, (const u64*)gk, level, ep, nb, w, S(s));
+        if (r) return r;
+    }
+    return HELR_OK;
+}
