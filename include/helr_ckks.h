@@ -141,22 +141,48 @@ int helr_refresh(helr_ctx* ctx, const uint64_t* sk, const uint64_t* a,
 
 /* ---- fused training step (enctrain.py:344-398 loop body) ---------------- */
 
-/* One enhanced-NAG iteration over one batch of `blocks` Z ciphertexts (one
- * column block), depth-7 schedule.  All constants are
- * per-limb residues prepared by the host planner:
- *   consts: u64[HELR_NAG_NCONST][L] (see DESIGN.md for the order)
- *   mask_pt: u64[L][N] row-start mask plaintext (NTT form)
- *   rot_keys: device pointers to the Galois keys, left steps 1..g/2, right
- *   steps 1..g/2, row steps g..S/2 (in that order).
- * w, v: in/out weight ciphertexts (level lw in, level lw-7 out).
- * bbar: quadratic-gradient scale ciphertext at level >= lw-5. */
+/* One enhanced-NAG iteration over one batch, depth-7 schedule:
+ *   P_r  = rescale(relin(sum_j Z_rj (x) W_j))                 level lw-1
+ *   R_r  = rotsum_left(P_r)  (log_g rotate-and-add)            (sum_col_vec, left half)
+ *   U_r  = rotsum_right(rescale(R_r * mask))                   level lw-2
+ *   QU_r = q0 + q1 U + q2 U^2 + q3 U^3 (U^2 and (q3 U) products) level lw-4
+ *   G_j  = rescale(relin(sum_r QU_r (x) Z_rj))                 level lw-5
+ *   G_j  = rotsum_rows(G_j) (log_m rotate-and-add by g*2^i)   (sum_rows)
+ *   D_j  = rescale(relin(G_j (x) Bbar_j))                      level lw-6
+ *   V'   = rescale(c_w1 W + c_a1 D);  W' = rescale(c_w2 W + c_v2 V + c_a2 D)  level lw-7
+ * Constants are per-limb residues prepared by the host planner
+ * (paper_2406_13221_b200/driver.py), consts[k*L + i] for k:
+ *   0 C3 (q3 u, level lw-2)   1 C1 (q1 u -> lw-4)   2 C2 (q2 u^2 -> lw-4)
+ *   3 C0 (q0 added at lw-4)   4 c_w1  5 c_a1  6 c_w2  7 c_v2  8 c_a2  9 unused
+ * Ciphertext arrays are contiguous u64[2][L][N] buffers. */
 #define HELR_NAG_NCONST 10
-int helr_nag_iteration(helr_ctx* ctx, const uint64_t* z, int blocks, int log_g,
-                       int log_m, const uint64_t* w, const uint64_t* v,
-                       const uint64_t* bbar, int bbar_level, int lw,
-                       const uint64_t* rlk, const uint64_t* const* rot_keys,
-                       const uint64_t* mask_pt, const uint64_t* consts,
-                       uint64_t* w_out, uint64_t* v_out, void* stream);
+typedef struct helr_nag_args {
+    const uint64_t* z;      /* [rows][cols] ciphertexts of this batch, level >= lw */
+    int rows, cols;         /* row blocks per batch, column blocks */
+    int log_g, log_m;       /* block of m = 2^log_m rows x g = 2^log_g columns, m*g = N/2 */
+    uint64_t* w;            /* [cols] weights: level lw in, level lw-7 out (in place) */
+    uint64_t* v;            /* [cols] companion weights, same */
+    const uint64_t* bbar;   /* [cols] quadratic-gradient scales, level >= lw-5 */
+    int lw;                 /* level of w and v on entry, >= 7 */
+    const uint64_t* rlk;    /* relinearisation key */
+    const uint64_t* const* rot_left;   /* [log_g] keys, left rotation by 2^i */
+    const uint64_t* const* rot_right;  /* [log_g] keys, right rotation by 2^i */
+    const uint64_t* const* rot_rows;   /* [log_m] keys, left rotation by g*2^i */
+    const uint64_t* mask_pt;           /* [L][N] row-start mask plaintext (NTT) */
+    const uint64_t* consts;            /* device [HELR_NAG_NCONST][L] */
+    uint64_t* grad;                    /* [cols] gradient accumulator (full batch) */
+    int phase;  /* 0: full mini-batch iteration; 1: grad = this batch's gradient;
+                   2: grad += this batch's gradient; 3: finish from grad (row sums,
+                   Bbar product, update) */
+} helr_nag_args;
+
+int helr_nag_iteration(helr_ctx* ctx, const helr_nag_args* args, void* stream);
+
+/* Capture / replay the iteration as a CUDA graph (same arguments each
+ * replay; constants are read from args->consts at replay time). */
+int helr_nag_graph_capture(helr_ctx* ctx, const helr_nag_args* args, void* stream, void** graph_exec);
+int helr_nag_graph_launch(void* graph_exec, void* stream);
+int helr_nag_graph_destroy(void* graph_exec);
 
 #ifdef __cplusplus
 }

@@ -519,6 +519,25 @@ void oc_keyswitch(oc_ctx* c, const u64* d, const u64* evk, int level, u64* k0, u
     free(pc); free(conv); free(acc);
 }
 
+/* tensor of one pair: d = [d0, d1, d2] (u64[3][L][N]) for limbs 0..level */
+void oc_tensor(oc_ctx* c, const u64* a, const u64* b, u64* d, int level) {
+    int N = c->n;
+    const int x = 0;
+#pragma omp parallel for
+    for (int p = 0; p <= level; p++) {
+        u64 q = c->prm[p];
+        const u64 *a0 = CT(a, x, 0, p), *a1 = CT(a, x, 1, p), *b0 = CT(b, x, 0, p), *b1 = CT(b, x, 1, p);
+        u64* d0 = d + (size_t)p * N;
+        u64* d1 = d + ((size_t)c->L + p) * N;
+        u64* d2 = d + ((size_t)2 * c->L + p) * N;
+        for (int i = 0; i < N; i++) {
+            d0[i] = mulm(a0[i], b0[i], q);
+            d1[i] = addm(mulm(a0[i], b1[i], q), mulm(a1[i], b0[i], q), q);
+            d2[i] = mulm(a1[i], b1[i], q);
+        }
+    }
+}
+
 /* ---------------- composite ops ---------------- */
 void oc_mul_relin(oc_ctx* c, const u64* a, const u64* b, const u64* rlk, u64* out, int count, int level) {
     int N = c->n, nl = level + 1;

@@ -65,6 +65,7 @@ def lib():
             "oc_rescale": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_int]),
             "oc_basis_convert": (None, [vp, _u64p, _intp, ctypes.c_int, _u64p, _intp, ctypes.c_int]),
             "oc_keyswitch": (None, [vp, _u64p, _u64p, ctypes.c_int, _u64p, _u64p]),
+            "oc_tensor": (None, [vp, _u64p, _u64p, _u64p, ctypes.c_int]),
             "oc_mul_relin": (None, [vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_int, ctypes.c_int]),
             "oc_automorph": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
             "oc_rotate": (None, [vp, _u64p, ctypes.c_int64, _u64p, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
@@ -220,6 +221,12 @@ class Oracle:
         k1 = np.zeros_like(k0)
         lib().oc_keyswitch(self._h, _p(d), _p(evk), level, _p(k0), _p(k1))
         return k0, k1
+
+    def tensor(self, a, b, level):
+        """[d0, d1, d2] of one ciphertext pair, u64[3][L][N]."""
+        d = np.zeros((3, self.L, self.N), dtype=np.uint64)
+        lib().oc_tensor(self._h, _p(np.ascontiguousarray(a)), _p(np.ascontiguousarray(b)), _p(d), level)
+        return d
 
     def mul_relin(self, a, b, rlk, level):
         out = self._out(a)

@@ -216,6 +216,17 @@ class GpuContext:
         self._call("helr_encrypt", _ptr(self.sk), _ptr(msg), _ptr(buf), count, level, self.enc_seed, first, _stream())
         return [self._wrap(buf[b], level, scale) for b in range(count)]
 
+    def encrypt_to(self, coef: np.ndarray, dest: torch.Tensor, level: int) -> None:
+        """Encrypt int64[B][N] coefficients into the contiguous device buffer
+        ``dest`` (B x [2][L][N]); randomness ids are taken from the context."""
+        coef = np.ascontiguousarray(np.atleast_2d(coef), dtype=np.int64)
+        count = coef.shape[0]
+        if not dest.is_contiguous() or dest.numel() != count * 2 * self.ckks.L * self.ckks.n:
+            raise ValueError("destination must be a contiguous batch of ciphertext buffers")
+        msg = torch.from_numpy(coef).to(self.device)
+        first = self._take_ct_ids(count)
+        self._call("helr_encrypt", _ptr(self.sk), _ptr(msg), _ptr(dest), count, level, self.enc_seed, first, _stream())
+
     def enc(self, message) -> GpuCiphertext:
         """Encrypt at most N/2 values, zero-padded (hesim.py:146-158)."""
         m = np.asarray(message, dtype=np.complex128).ravel()

@@ -8,7 +8,7 @@
 #pragma once
 #include <cstdint>
 
-typedef unsigned long long u64;
+typedef uint64_t u64;
 typedef unsigned int u32;
 
 #define HD __host__ __device__ __forceinline__

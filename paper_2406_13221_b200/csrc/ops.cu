@@ -16,6 +16,7 @@
 
 #include "../../include/helr_ckks.h"
 #include "ntt.cuh"
+#include "ops_internal.cuh"
 
 #define CHECK_LAUNCH(what)                                              \
     do {                                                                \
@@ -38,8 +39,8 @@ __device__ __forceinline__ int galois_perm(int i, u64 g, int log_n) {
 // elementwise kernels.  Items are ciphertexts (2 polys) unless noted; index
 // space: (item, poly, limb, n) flattened with limbs 0..level.
 struct EwGeom {
-    int n, log_n, L, nl;  // nl = level+1 active limbs
-    long long item_stride;  // words between ciphertexts
+    int n, log_n, L, nl;      // nl = level+1 active limbs
+    long long as, bs, os;     // item strides (words) of a, b (ciphertext operands), out
 };
 __device__ __forceinline__ void ew_decode(long long idx, const EwGeom& g, int& item, int& poly, int& limb, int& k) {
     k = (int)(idx & (g.n - 1));
@@ -49,11 +50,7 @@ __device__ __forceinline__ void ew_decode(long long idx, const EwGeom& g, int& i
     poly = (int)(r & 1);
     item = (int)(r >> 1);
 }
-__device__ __forceinline__ size_t ew_off(const EwGeom& g, int item, int poly, int limb, int k) {
-    return (size_t)item * g.item_stride + ((size_t)poly * g.L + limb) * g.n + k;
-}
 
-enum EwOp { EW_ADD = 0, EW_SUB, EW_ADDC, EW_ADDPT, EW_MULC, EW_MULPT, EW_IMUL };
 
 __global__ void k_elementwise(int op, const u64* a, const u64* b, u64* out, EwGeom g, long long total,
                               Tables tb, const u64* imul_f) {
@@ -62,32 +59,38 @@ __global__ void k_elementwise(int op, const u64* a, const u64* b, u64* out, EwGe
         int item, poly, limb, k;
         ew_decode(idx, g, item, poly, limb, k);
         const u64 q = tb.q[limb];
-        const size_t o = ew_off(g, item, poly, limb, k);
-        const u64 x = a[o];
+        const size_t in_poly = ((size_t)poly * g.L + limb) * g.n + k;
+        const u64 x = a[(size_t)item * g.as + in_poly];
         u64 r;
         switch (op) {
-            case EW_ADD: r = add_mod(x, b[o], q); break;
-            case EW_SUB: r = sub_mod(x, b[o], q); break;
+            case EW_ADD: r = add_mod(x, b[(size_t)item * g.bs + in_poly], q); break;
+            case EW_SUB: r = sub_mod(x, b[(size_t)item * g.bs + in_poly], q); break;
             case EW_ADDC: r = poly == 0 ? add_mod(x, b[limb], q) : x; break;
             case EW_ADDPT: r = poly == 0 ? add_mod(x, b[(size_t)limb * g.n + k], q) : x; break;
             case EW_MULC: r = mul_mod(x, b[limb], q, tb.br1[limb], tb.br0[limb]); break;
             case EW_MULPT: r = mul_mod(x, b[(size_t)limb * g.n + k], q, tb.br1[limb], tb.br0[limb]); break;
             default: r = mul_mod(x, imul_f[(size_t)limb * g.n + k], q, tb.br1[limb], tb.br0[limb]); break;
         }
-        out[o] = r;
+        out[(size_t)item * g.os + in_poly] = r;
     }
 }
 
-static int launch_ew(helr_ctx* c, int op, const u64* a, const u64* b, u64* out, int count, int level, void* s) {
+int op_ew(helr_ctx* c, int op, const u64* a, long long as, const u64* b, long long bs, u64* out, long long os,
+          int count, int level, cudaStream_t s) {
     if (level < 0 || level >= c->L || count < 0) { set_error("bad level/count"); return HELR_EINVAL; }
     if (count == 0) return HELR_OK;
-    EwGeom g{c->n, c->log_n, c->L, level + 1, 2ll * c->L * c->n};
+    EwGeom g{c->n, c->log_n, c->L, level + 1, as, bs, os};
     long long total = (long long)count * 2 * (level + 1) * c->n;
     int blocks = blocks_for(total, 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_elementwise<<<blocks, 256, 0, S(s)>>>(op, a, b, out, g, total, c->t, c->imul_f);
+    k_elementwise<<<blocks, 256, 0, s>>>(op, a, b, out, g, total, c->t, c->imul_f);
     CHECK_LAUNCH("elementwise");
     return HELR_OK;
+}
+
+static int launch_ew(helr_ctx* c, int op, const u64* a, const u64* b, u64* out, int count, int level, void* s) {
+    const long long cs = 2ll * c->L * c->n;
+    return op_ew(c, op, a, cs, b, cs, out, cs, count, level, S(s));
 }
 
 extern "C" int helr_add(helr_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, int count, int level, void* s) {
@@ -351,27 +354,37 @@ __global__ void k_rescale_conv(const u64* r, u64* t, int n, int l, Tables tb) {
         }
     }
 }
-__global__ void k_rescale_final(const u64* x, const u64* t, u64* out, int n, int L, int l, const u64* qlinv,
-                                const u64* qlinv_sh, Tables tb) {
+__global__ void k_rescale_final(const u64* x, long long xs, const u64* t, u64* out, long long os, int n, int L, int l,
+                                const u64* qlinv, const u64* qlinv_sh, Tables tb) {
     const int it = blockIdx.z, p = blockIdx.y;  // it = item*2 + poly
+    const int item = it >> 1, poly = it & 1;
     const u64 q = tb.q[p];
     const u64 w = qlinv[(size_t)l * L + p], wsh = qlinv_sh[(size_t)l * L + p];
-    const u64* xp = x + ((size_t)it * L + p) * n;
+    const u64* xp = x + (size_t)item * xs + ((size_t)poly * L + p) * n;
     const u64* tp = t + ((size_t)it * l + p) * n;
-    u64* op = out + ((size_t)it * L + p) * n;
+    u64* op = out + (size_t)item * os + ((size_t)poly * L + p) * n;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         op[i] = shoup(sub_mod(xp[i], tp[i], q), w, wsh, q);
 }
 
-static int rescale_dev(helr_ctx* c, const u64* a, u64* out, int count, int level, cudaStream_t s) {
+// polynomial (item, poly) of a strided ciphertext batch, limb `li` offset added by the caller
+struct LdPolyLimb {
+    const u64* base;   // points at limb l of poly 0 of item 0
+    long long item_stride, poly_stride;
+    __device__ __forceinline__ u64 operator()(int z, int, int, int off) const {
+        return base[(size_t)(z >> 1) * item_stride + (size_t)(z & 1) * poly_stride + off];
+    }
+};
+
+static int rescale_dev(helr_ctx* c, const u64* a, long long as, u64* out, long long os, int count, int level,
+                       cudaStream_t s) {
     const int n = c->n, L = c->L, l = level;
     const int items = 2 * count;  // polynomials
     u64* r = c->ws;                                // [items][N]
     u64* t = c->ws + (size_t)items * n;            // [items][l][N]
-    // r = INTT(limb l) per polynomial (polynomial stride L*N)
     {
         LimbMap m; m.count = 1; m.off[0] = 0; m.prime[0] = (unsigned char)l;
-        LdBuf ld{a + (size_t)l * n, (long long)L * n, m, n};
+        LdPolyLimb ld{a + (size_t)l * n, as, (long long)L * n};
         StBuf st{r, (long long)n, m, n};
         ntt_launch<true>(c, ld, st, r, n, m, items, s);
         CHECK_LAUNCH("rescale intt");
@@ -383,23 +396,27 @@ static int rescale_dev(helr_ctx* c, const u64* a, u64* out, int count, int level
     ntt_buffers<false>(c, t, (long long)l * n, t, (long long)l * n, m, items, s);
     CHECK_LAUNCH("rescale ntt");
     dim3 g2(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, l, items);
-    k_rescale_final<<<g2, 256, 0, s>>>(a, t, out, n, L, l, c->qlinv, c->qlinv_sh, c->t);
+    k_rescale_final<<<g2, 256, 0, s>>>(a, as, t, out, os, n, L, l, c->qlinv, c->qlinv_sh, c->t);
     CHECK_LAUNCH("rescale final");
     return HELR_OK;
 }
 
-extern "C" int helr_rescale(helr_ctx* c, const uint64_t* a, uint64_t* out, int count, int level, void* s) {
+int op_rescale(helr_ctx* c, const u64* a, long long as, u64* out, long long os, int count, int level, cudaStream_t s) {
     if (level < 1 || level >= c->L) { set_error("rescale needs level >= 1"); return HELR_EINVAL; }
     const size_t need = (size_t)2 * (level + 1) * c->n;  // per ciphertext (r + t)
     int chunk = (int)(c->ws_words / need);
     if (chunk < 1) { set_error("workspace too small"); return HELR_ENOMEM; }
     for (int b0 = 0; b0 < count; b0 += chunk) {
         int nb = count - b0 < chunk ? count - b0 : chunk;
-        size_t off = (size_t)b0 * 2 * c->L * c->n;
-        int r = rescale_dev(c, (const u64*)a + off, (u64*)out + off, nb, level, S(s));
+        int r = rescale_dev(c, a + (size_t)b0 * as, as, out + (size_t)b0 * os, os, nb, level, s);
         if (r) return r;
     }
     return HELR_OK;
+}
+
+extern "C" int helr_rescale(helr_ctx* c, const uint64_t* a, uint64_t* out, int count, int level, void* s) {
+    const long long cs = 2ll * c->L * c->n;
+    return op_rescale(c, (const u64*)a, cs, (u64*)out, cs, count, level, S(s));
 }
 
 // ---------------------------------------------------------------------------
@@ -667,42 +684,83 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
     return HELR_OK;
 }
 
-// tensor: d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1   (into [B][3][L][N])
-__global__ void k_tensor(const u64* a, const u64* b, u64* d, int n, int L, int nl, Tables tb) {
+// tensor sum: d = sum_t a_t (x) b_t  (d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1) into [B][3][L][N]
+struct TensorArgs {
+    const u64* a; long long a_is, a_ts;
+    const u64* b; long long b_is, b_ts;
+    int terms;
+};
+__global__ void k_tensor(TensorArgs ta, u64* d, int n, int L, Tables tb) {
     const int p = blockIdx.y, it = blockIdx.z;
     const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
-    const u64* a0 = a + (size_t)it * 2 * L * n + (size_t)p * n;
-    const u64* a1 = a0 + (size_t)L * n;
-    const u64* b0 = b + (size_t)it * 2 * L * n + (size_t)p * n;
-    const u64* b1 = b0 + (size_t)L * n;
     u64* d0 = d + (size_t)it * 3 * L * n + (size_t)p * n;
     u64* d1 = d0 + (size_t)L * n;
     u64* d2 = d1 + (size_t)L * n;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const u64 x0 = a0[i], x1 = a1[i], y0 = b0[i], y1 = b1[i];
-        d0[i] = mul_mod(x0, y0, q, r1, r0);
-        u128v m = mul_wide(x0, y1);
-        acc_wide(m, x1, y0);
-        d1[i] = barrett128(m, q, r1, r0);
-        d2[i] = mul_mod(x1, y1, q, r1, r0);
+        u128v s0{0, 0}, s1{0, 0}, s2{0, 0};
+        for (int t = 0; t < ta.terms; t++) {
+            const u64* a0 = ta.a + (size_t)it * ta.a_is + (size_t)t * ta.a_ts + (size_t)p * n;
+            const u64* b0 = ta.b + (size_t)it * ta.b_is + (size_t)t * ta.b_ts + (size_t)p * n;
+            const u64 x0 = a0[i], x1 = a0[(size_t)L * n + i], y0 = b0[i], y1 = b0[(size_t)L * n + i];
+            acc_wide(s0, x0, y0);
+            acc_wide(s1, x0, y1);
+            acc_wide(s1, x1, y0);
+            acc_wide(s2, x1, y1);
+            if ((t & 1) == 1 && t + 1 < ta.terms) {
+                s0 = u128v{0, barrett128(s0, q, r1, r0)};
+                s1 = u128v{0, barrett128(s1, q, r1, r0)};
+                s2 = u128v{0, barrett128(s2, q, r1, r0)};
+            }
+        }
+        d0[i] = barrett128(s0, q, r1, r0);
+        d1[i] = barrett128(s1, q, r1, r0);
+        d2[i] = barrett128(s2, q, r1, r0);
     }
 }
 
-extern "C" int helr_mul_relin(helr_ctx* c, const uint64_t* a, const uint64_t* b, const uint64_t* rlk, uint64_t* out,
-                              int count, int level, void* s) {
+int op_mul_relin_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, const u64* b, long long b_is,
+                     long long b_ts, int terms, const u64* rlk, u64* out, long long os, int count, int level,
+                     cudaStream_t s) {
     if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    if (terms < 1) { set_error("need at least one product term"); return HELR_EINVAL; }
     const int chunk = c->max_batch;
-    const long long cs = 2ll * c->L * c->n;
     for (int b0 = 0; b0 < count; b0 += chunk) {
         int nb = count - b0 < chunk ? count - b0 : chunk;
         KsWs w = ks_ws(c, chunk);
         dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, nb);
-        k_tensor<<<g, 256, 0, S(s)>>>((const u64*)a + b0 * cs, (const u64*)b + b0 * cs, w.tensor, c->n, c->L, level + 1, c->t);
+        TensorArgs ta{a + (size_t)b0 * a_is, a_is, a_ts, b + (size_t)b0 * b_is, b_is, b_ts, terms};
+        k_tensor<<<g, 256, 0, s>>>(ta, w.tensor, c->n, c->L, c->t);
         CHECK_LAUNCH("tensor");
         const long long ts = 3ll * c->L * c->n;
         KsInput in{w.tensor + 2ll * c->L * c->n, ts, 0};
-        KsEpilogue ep{(u64*)out + b0 * cs, cs, w.tensor, ts, nullptr, 0, 0};
-        int r = keyswitch_batch(c, in, (const u64*)rlk, level, ep, nb, w, S(s));
+        KsEpilogue ep{out + (size_t)b0 * os, os, w.tensor, ts, nullptr, 0, 0};
+        int r = keyswitch_batch(c, in, rlk, level, ep, nb, w, s);
+        if (r) return r;
+    }
+    return HELR_OK;
+}
+
+extern "C" int helr_mul_relin(helr_ctx* c, const uint64_t* a, const uint64_t* b, const uint64_t* rlk, uint64_t* out,
+                              int count, int level, void* s) {
+    const long long cs = 2ll * c->L * c->n;
+    return op_mul_relin_sum(c, (const u64*)a, cs, 0, (const u64*)b, cs, 0, 1, (const u64*)rlk, (u64*)out, cs, count,
+                            level, S(s));
+}
+
+int op_rotate(helr_ctx* c, const u64* a, long long as, long long galois, const u64* gk, u64* out, long long os,
+              int count, int level, int accumulate, cudaStream_t s) {
+    if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    if (galois <= 0 || (galois & 1) == 0) { set_error("galois element must be odd and positive"); return HELR_EINVAL; }
+    if (a == out) { set_error("rotate: out must not alias the input"); return HELR_EINVAL; }
+    const int chunk = c->max_batch;
+    const long long g = (long long)(galois % (2ll * c->n));
+    for (int b0 = 0; b0 < count; b0 += chunk) {
+        int nb = count - b0 < chunk ? count - b0 : chunk;
+        KsWs w = ks_ws(c, chunk);
+        const u64* ab = a + (size_t)b0 * as;
+        KsInput in{ab + (size_t)c->L * c->n, as, g};
+        KsEpilogue ep{out + (size_t)b0 * os, os, accumulate ? ab : nullptr, as, ab, as, g};
+        int r = keyswitch_batch(c, in, gk, level, ep, nb, w, s);
         if (r) return r;
     }
     return HELR_OK;
@@ -710,20 +768,43 @@ extern "C" int helr_mul_relin(helr_ctx* c, const uint64_t* a, const uint64_t* b,
 
 extern "C" int helr_rotate(helr_ctx* c, const uint64_t* a, int64_t galois, const uint64_t* gk, uint64_t* out, int count,
                            int level, int accumulate, void* s) {
-    if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
-    if (galois <= 0 || (galois & 1) == 0) { set_error("galois element must be odd and positive"); return HELR_EINVAL; }
-    if (a == out) { set_error("helr_rotate: out must not alias the input"); return HELR_EINVAL; }
-    const int chunk = c->max_batch;
     const long long cs = 2ll * c->L * c->n;
-    const long long g = (long long)(galois % (2ll * c->n));
-    for (int b0 = 0; b0 < count; b0 += chunk) {
-        int nb = count - b0 < chunk ? count - b0 : chunk;
-        KsWs w = ks_ws(c, chunk);
-        const u64* ab = (const u64*)a + b0 * cs;
-        KsInput in{ab + (size_t)c->L * c->n, cs, g};
-        KsEpilogue ep{(u64*)out + b0 * cs, cs, accumulate ? ab : nullptr, cs, ab, cs, g};
-        int r = keyswitch_batch(c, in, (const u64*)gk, level, ep, nb, w, S(s));
-        if (r) return r;
+    return op_rotate(c, (const u64*)a, cs, (long long)galois, (const u64*)gk, (u64*)out, cs, count, level, accumulate,
+                     S(s));
+}
+
+// out = sum_t C_t * X_t  (per-limb constants, both polynomials), no rescale
+struct LinArgs {
+    const u64* x[4];
+    long long xs[4];
+    const u64* k[4];
+    int terms;
+};
+__global__ void k_lincomb(LinArgs la, u64* out, long long os, int n, int L, Tables tb) {
+    const int p = blockIdx.y, it = blockIdx.z;  // it = item*2 + poly
+    const int item = it >> 1, poly = it & 1;
+    const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
+    u64* op = out + (size_t)item * os + ((size_t)poly * L + p) * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        u128v acc{0, 0};
+        for (int t = 0; t < la.terms; t++)
+            acc_wide(acc, la.x[t][(size_t)item * la.xs[t] + ((size_t)poly * L + p) * n + i], la.k[t][p]);
+        op[i] = barrett128(acc, q, r1, r0);
     }
+}
+
+int op_lincomb(helr_ctx* c, int terms, const u64* const* x, const long long* xs, const u64* const* k, u64* out,
+               long long os, int count, int level, cudaStream_t s) {
+    if (terms < 1 || terms > 4) { set_error("lincomb: 1..4 terms"); return HELR_EINVAL; }
+    LinArgs la;
+    for (int t = 0; t < 4; t++) {
+        la.x[t] = t < terms ? x[t] : nullptr;
+        la.xs[t] = t < terms ? xs[t] : 0;
+        la.k[t] = t < terms ? k[t] : nullptr;
+    }
+    la.terms = terms;
+    dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, 2 * count);
+    k_lincomb<<<g, 256, 0, s>>>(la, out, os, c->n, c->L, c->t);
+    CHECK_LAUNCH("lincomb");
     return HELR_OK;
 }

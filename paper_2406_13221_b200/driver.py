@@ -1,0 +1,380 @@
+"""Fused training driver: the reference's ``train_encrypted`` loop
+(enctrain.py:303-449) with each iteration issued as one native call
+(``helr_nag_iteration``) over a whole batch of row blocks, optionally
+replayed from a captured CUDA graph.
+
+Host responsibilities (this module):
+- ``plan_iteration``: exact-scale bookkeeping for the depth-7 schedule and
+  the per-limb integer constants it needs.  All scales are
+  fp64 and tracked exactly; every constant product encodes its constant at
+  the scale that makes the product land on a chosen target, so additions
+  always see equal scales.
+- ``FusedTrainer``: client preparation (pack + encrypt Z and B̄ on the
+  device), keys, the refresh policy (same arithmetic as
+  ``bootstrap_policy``, enctrain.py:242-255), decryption of the weights.
+
+Device responsibilities: everything between the weights going in and the
+updated weights coming out (csrc/nag.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .ckks import GpuContext
+from .encoding import BlockLayout, pack_matrix_array, plan_layout, replicate_rows
+from .optimizer import ALPHA0_INIT, BASELINE_CUBIC, PolyApprox, lr_at, merge_bbar, next_alpha, scaler_for
+
+__all__ = ["IterPlan", "plan_iteration", "NagArgs", "FusedTrainer", "NCONST", "ITER_DEPTH"]
+
+NCONST = 10
+ITER_DEPTH = 7  # rescales per iteration
+
+
+class NagArgs(ctypes.Structure):
+    """Mirror of ``helr_nag_args`` (include/helr_ckks.h)."""
+
+    _fields_ = [
+        ("z", ctypes.c_void_p), ("rows", ctypes.c_int), ("cols", ctypes.c_int),
+        ("log_g", ctypes.c_int), ("log_m", ctypes.c_int),
+        ("w", ctypes.c_void_p), ("v", ctypes.c_void_p), ("bbar", ctypes.c_void_p), ("lw", ctypes.c_int),
+        ("rlk", ctypes.c_void_p),
+        ("rot_left", ctypes.POINTER(ctypes.c_void_p)), ("rot_right", ctypes.POINTER(ctypes.c_void_p)),
+        ("rot_rows", ctypes.POINTER(ctypes.c_void_p)),
+        ("mask_pt", ctypes.c_void_p), ("consts", ctypes.c_void_p), ("grad", ctypes.c_void_p),
+        ("phase", ctypes.c_int),
+    ]
+
+
+def _bind(lib):
+    if getattr(lib, "_nag_bound", False):
+        return
+    lib.helr_nag_iteration.argtypes = [ctypes.c_void_p, ctypes.POINTER(NagArgs), ctypes.c_void_p]
+    lib.helr_nag_iteration.restype = ctypes.c_int
+    lib.helr_nag_graph_capture.argtypes = [ctypes.c_void_p, ctypes.POINTER(NagArgs), ctypes.c_void_p,
+                                           ctypes.POINTER(ctypes.c_void_p)]
+    lib.helr_nag_graph_capture.restype = ctypes.c_int
+    lib.helr_nag_graph_launch.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    lib.helr_nag_graph_launch.restype = ctypes.c_int
+    lib.helr_nag_graph_destroy.argtypes = [ctypes.c_void_p]
+    lib.helr_nag_graph_destroy.restype = ctypes.c_int
+    lib._nag_bound = True
+
+
+# ---------------------------------------------------------------- planning
+@dataclass
+class IterPlan:
+    lw: int
+    consts: np.ndarray          # uint64 [NCONST][L]
+    ints: list                  # the signed integer constants (for the oracle)
+    mask_scale: float
+    s_out: float
+    scales: dict = field(default_factory=dict)
+
+
+def _rint(x: float) -> int:
+    return int(np.rint(x))
+
+
+def plan_iteration(ck, lw: int, s_w: float, s_v: float, s_z: float, s_b: float, qpoly, mult: float,
+                   eta: float) -> IterPlan:
+    """Constants of one depth-7 iteration starting with W, V at level ``lw``.
+
+    qpoly = (q0, q1, q2, q3): coefficients of 1 - sigmoid_poly (the
+    complement, enctrain.py:155-159, sigmoid.py:72-76); mult = 1 + gamma
+    (enhanced) or gamma (baseline), eta = (1 - alpha0) / alpha1
+    (enctrain.py:362-366, 224-229).
+    """
+    if lw < ITER_DEPTH or lw >= ck.L:
+        raise ValueError(f"iteration needs W at a level in [{ITER_DEPTH}, {ck.L}), got {lw}")
+    q = [float(x) for x in ck.q]
+    D = ck.level_scales
+    l = lw
+    q0, q1, q2, q3 = qpoly
+    s_p = s_z * s_w / q[l]
+    s_u = D[l - 2]
+    mask_scale = s_u * q[l - 1] / s_p
+    s_u2 = s_u * s_u / q[l - 2]
+    s_s = D[l - 5]
+    s_c = s_s * q[l - 4] / s_z
+    s_t = s_c * q[l - 3] / s_u2
+    c3 = _rint(q3 * s_t * q[l - 2] / s_u)
+    c1 = _rint(q1 * s_c * q[l - 3] / s_u)
+    c2 = _rint(q2 * s_c * q[l - 3] / s_u2)
+    c0 = _rint(q0 * s_c)
+    s_d = s_s * s_b / q[l - 5]
+    s_out = D[l - 7]
+    f = s_out * q[l - 6]
+    cw1 = _rint(f / s_w)
+    ca1 = _rint(mult * f / s_d)
+    cw2 = _rint((1.0 - eta) * f / s_w)
+    cv2 = _rint(eta * f / s_v)
+    ca2 = _rint((1.0 - eta) * mult * f / s_d)
+    ints = [c3, c1, c2, c0, cw1, ca1, cw2, cv2, ca2, 0]
+    consts = np.zeros((NCONST, ck.L), dtype=np.uint64)
+    for k, v in enumerate(ints):
+        consts[k] = [v % p for p in ck.q]
+    return IterPlan(lw=lw, consts=consts, ints=ints, mask_scale=mask_scale, s_out=s_out,
+                    scales=dict(p=s_p, u=s_u, u2=s_u2, c=s_c, s=s_s, d=s_d, out=s_out))
+
+
+def row_mask(slots: int, g: int) -> np.ndarray:
+    m = np.zeros(slots)
+    m[::g] = 1.0
+    return m
+
+
+# ---------------------------------------------------------------- trainer
+class FusedTrainer:
+    """Encrypted enhanced-NAG logistic regression on one GPU.
+
+    Packing: each block is m x g (m rows, g = S/m columns); a batch is
+    ``blocks_per_batch`` consecutive row blocks (the BASELINE paper shape
+    packs a 1,024-row batch as 8 blocks of 128 x 256); ``cols`` column
+    blocks cover the f+1 coefficients.  Mini-batch mode visits one batch
+    per iteration in order; full-batch mode sums every batch's gradient
+    before one B̄ product and update (enctrain.py:356-359, 374-381).
+    """
+
+    def __init__(self, ctx: GpuContext, ds, rows_per_block: int, blocks_per_batch: int = 1,
+                 mode: str = "mini_batch", poly: PolyApprox = BASELINE_CUBIC, schedule=None,
+                 epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False,
+                 z_on_host: bool = False):
+        if mode not in ("mini_batch", "full_batch"):
+            raise ValueError(f"mode must be mini_batch or full_batch, got {mode!r}")
+        from .optimizer import ExpDecay
+        self.ctx = ctx
+        self.ck = ctx.ckks
+        self.ds = ds
+        self.mode = mode
+        self.poly = poly
+        self.schedule = schedule if schedule is not None else ExpDecay()
+        self.epsilon = epsilon
+        self.enhanced = enhanced
+        self.use_graph = use_graph
+        self.layout: BlockLayout = plan_layout(ds.n_samples, ds.n_features, ctx.params, rows_per_block)
+        lay = self.layout
+        self.rows = blocks_per_batch
+        self.cols = lay.col_blocks
+        self.n_batches = -(-lay.row_blocks // blocks_per_batch)
+        self.log_g = int(math.log2(lay.g))
+        self.log_m = int(math.log2(lay.m))
+        self.batch_rows = lay.m * blocks_per_batch
+        self.qpoly = poly.complement().padded(3)
+        self.lib = _lib.load()
+        _bind(self.lib)
+        self._graph = None
+        self._graph_key = None
+        self.timings: dict = {}
+        self.z_on_host = z_on_host
+        self._prepare()
+
+    # ------------------------------------------------------------ client side
+    def _prepare(self):
+        ctx, ck, lay, ds = self.ctx, self.ck, self.layout, self.ds
+        t0 = time.perf_counter()
+        Z = ds.X * ds.y[:, None]
+        blocks = pack_matrix_array(Z, lay)                       # (row_blocks, cols, S)
+        nb, R, C = self.n_batches, self.rows, self.cols
+        full = np.zeros((nb * R, C, ck.slots))
+        full[: lay.row_blocks] = blocks
+        top = ck.top_level
+        s_top = ck.level_scales[top]
+        L, N = ck.L, ck.n
+        store_dev = "cpu" if self.z_on_host else ctx.device
+        self.z = torch.empty((nb, R, C, 2, L, N), dtype=torch.int64, device=store_dev,
+                             pin_memory=bool(self.z_on_host))
+        chunk = 64
+        flat = full.reshape(nb * R * C, ck.slots)
+        zflat = self.z.view(nb * R * C, 2, L, N)
+        stage = None if not self.z_on_host else torch.empty((chunk, 2, L, N), dtype=torch.int64, device=ctx.device)
+        for s in range(0, flat.shape[0], chunk):
+            coef = ctx.encoder.encode(flat[s:s + chunk], s_top)
+            if self.z_on_host:
+                ctx.encrypt_to(coef, stage[: coef.shape[0]], top)
+                zflat[s:s + coef.shape[0]].copy_(stage[: coef.shape[0]])
+            else:
+                ctx.encrypt_to(coef, zflat[s:s + coef.shape[0]], top)
+        self.s_z = s_top
+        # B̄: one per batch (mini) or merged over batches (full); computed on
+        # the real rows of each batch (enctrain.py:132-142, BASELINE "per batch")
+        scalers = []
+        for b in range(nb):
+            lo = b * self.batch_rows
+            hi = min(lo + self.batch_rows, ds.n_samples)
+            scalers.append(scaler_for(ds.X[lo:hi], self.epsilon))
+        self.scalers = scalers
+        if self.mode == "full_batch":
+            vecs = [merge_bbar(scalers).b]
+        else:
+            vecs = [s.b for s in scalers]
+        bb = np.stack([np.stack(replicate_rows(v, lay)) for v in vecs])   # (nbb, C, S)
+        self.bbar = torch.empty((bb.shape[0], C, 2, L, N), dtype=torch.int64, device=ctx.device)
+        bflat = bb.reshape(-1, ck.slots)
+        out = self.bbar.view(-1, 2, L, N)
+        for s in range(0, bflat.shape[0], chunk):
+            coef = ctx.encoder.encode(bflat[s:s + chunk], s_top)
+            ctx.encrypt_to(coef, out[s:s + coef.shape[0]], top)
+        self.s_b = s_top
+        # W0 = V0 = enc(0) at the top level (enctrain.py:145-151)
+        self.wv = torch.empty((2 * C, 2, L, N), dtype=torch.int64, device=ctx.device)
+        ctx.encrypt_to(np.zeros((2 * C, N), dtype=np.int64), self.wv, top)
+        self.level = top
+        self.s_w = self.s_v = s_top
+        self.alpha0 = ALPHA0_INIT
+        self.alpha1 = next_alpha(ALPHA0_INIT)
+        self.t = 0
+        # keys: left/right 2^i (sum_col_vec), g*2^i (sum_rows)
+        S = ck.slots
+        self.gal_left = [pow(5, 1 << i, 2 * N) for i in range(self.log_g)]
+        self.gal_right = [pow(5, S - (1 << i), 2 * N) for i in range(self.log_g)]
+        self.gal_rows = [pow(5, lay.g << i, 2 * N) for i in range(self.log_m)]
+        keys = lambda gs: (ctypes.c_void_p * max(1, len(gs)))(*[ctx.galois_key(g).data_ptr() for g in gs])
+        self._k_left, self._k_right, self._k_rows = keys(self.gal_left), keys(self.gal_right), keys(self.gal_rows)
+        self._masks: dict = {}
+        self.consts_dev = torch.zeros((NCONST, L), dtype=torch.int64, device=ctx.device)
+        self.consts_host = torch.zeros((NCONST, L), dtype=torch.int64, pin_memory=True)
+        self.grad = torch.empty((C, 2, L, N), dtype=torch.int64, device=ctx.device)
+        self.zstage = None
+        if self.z_on_host:
+            self.zstage = torch.empty((R, C, 2, L, N), dtype=torch.int64, device=ctx.device)
+        torch.cuda.synchronize()
+        self.timings["prepare_s"] = time.perf_counter() - t0
+
+    def _mask(self, lw: int, scale: float) -> torch.Tensor:
+        key = (lw, round(scale))
+        if key not in self._masks:
+            ck = self.ck
+            coef = self.ctx.encoder.encode(row_mask(ck.slots, self.layout.g), scale)
+            self._masks[key] = self.ctx._plain(coef, lw - 1)
+        return self._masks[key]
+
+    # ------------------------------------------------------------ iteration
+    def step_scalars(self, t: int, gamma_rows: int):
+        lr = lr_at(self.schedule, t)
+        eta = (1.0 - self.alpha0) / self.alpha1
+        gamma = lr / gamma_rows if self.enhanced else lr / self.ds.n_samples
+        mult = (1.0 + gamma) if self.enhanced else gamma
+        return lr, eta, gamma, mult
+
+    def _refresh_if_needed(self) -> bool:
+        # bootstrap_policy (enctrain.py:242-255): refresh when the next
+        # iteration cannot fit; one iteration consumes ITER_DEPTH limbs.
+        if self.level >= ITER_DEPTH:
+            return False
+        self.refresh()
+        return True
+
+    def refresh(self):
+        ck = self.ck
+        top = ck.top_level
+        ratio = ck.level_scales[top] / self.s_w
+        out = torch.empty_like(self.wv)
+        first = self.ctx._take_ct_ids(self.wv.shape[0])
+        self.ctx._call("helr_refresh", self.ctx.sk.data_ptr(), self.wv.data_ptr(), self.level, float(ratio),
+                       out.data_ptr(), top, self.wv.shape[0], self.ctx.enc_seed, first,
+                       torch.cuda.current_stream().cuda_stream)
+        self.wv = out
+        self.level = top
+        self.s_w = self.s_v = ck.level_scales[top]
+        self._graph_key = None  # pointers changed
+
+    def _args(self, z_ptr: int, bbar_ptr: int, plan: IterPlan, phase: int) -> NagArgs:
+        C = self.cols
+        cs = self.wv[0].numel() * 8
+        return NagArgs(z=z_ptr, rows=self.rows, cols=C, log_g=self.log_g, log_m=self.log_m,
+                       w=self.wv.data_ptr(), v=self.wv.data_ptr() + C * cs, bbar=bbar_ptr, lw=plan.lw,
+                       rlk=self.ctx.rlk.data_ptr(), rot_left=self._k_left, rot_right=self._k_right,
+                       rot_rows=self._k_rows, mask_pt=self._mask(plan.lw, plan.mask_scale).data_ptr(),
+                       consts=self.consts_dev.data_ptr(), grad=self.grad.data_ptr(), phase=phase)
+
+    def _upload_consts(self, plan: IterPlan):
+        self.consts_host.copy_(torch.from_numpy(plan.consts.view(np.int64)))
+        self.consts_dev.copy_(self.consts_host, non_blocking=True)
+
+    def _z_ptr(self, b: int) -> int:
+        if self.z_on_host:
+            self.zstage.copy_(self.z[b], non_blocking=True)
+            return self.zstage.data_ptr()
+        return self.z[b].data_ptr()
+
+    def _run(self, args: NagArgs):
+        stream = torch.cuda.current_stream().cuda_stream
+        if not self.use_graph:
+            _lib.check(self.lib.helr_nag_iteration(self.ctx.handle, ctypes.byref(args), stream), "helr_nag_iteration")
+            return
+        key = (args.z, args.w, args.bbar, args.lw, args.phase, args.mask_pt)
+        if self._graph is None or self._graph_key != key:
+            if self._graph is not None:
+                self.lib.helr_nag_graph_destroy(self._graph)
+                self._graph = None
+            # one eager run first allocates the driver workspace outside capture
+            if not getattr(self, "_warm", False):
+                _lib.check(self.lib.helr_nag_iteration(self.ctx.handle, ctypes.byref(args), stream),
+                           "helr_nag_iteration")
+                self._warm = True
+                return
+            g = ctypes.c_void_p()
+            _lib.check(self.lib.helr_nag_graph_capture(self.ctx.handle, ctypes.byref(args), stream, ctypes.byref(g)),
+                       "helr_nag_graph_capture")
+            self._graph, self._graph_key = g, key
+        _lib.check(self.lib.helr_nag_graph_launch(self._graph, stream), "helr_nag_graph_launch")
+
+    def iterate(self, batch: Optional[int] = None) -> dict:
+        """One NAG iteration (mini-batch: batch ``t mod n_batches``; full: all)."""
+        refreshed = self._refresh_if_needed()
+        if self.mode == "mini_batch":
+            b = (self.t % self.n_batches) if batch is None else batch
+            lo = b * self.batch_rows
+            gamma_rows = min(self.batch_rows, self.ds.n_samples - lo)
+        else:
+            gamma_rows = self.ds.n_samples
+        lr, eta, gamma, mult = self.step_scalars(self.t, gamma_rows)
+        plan = plan_iteration(self.ck, self.level, self.s_w, self.s_v, self.s_z, self.s_b, self.qpoly, mult, eta)
+        self._upload_consts(plan)
+        cs = self.bbar[0, 0].numel() * 8
+        if self.mode == "mini_batch":
+            args = self._args(self._z_ptr(b), self.bbar[b].data_ptr(), plan, 0)
+            self._run(args)
+        else:
+            for bb in range(self.n_batches):
+                args = self._args(self._z_ptr(bb), self.bbar[0].data_ptr(), plan, 1 if bb == 0 else 2)
+                self._run(args)
+            args = self._args(self._z_ptr(0), self.bbar[0].data_ptr(), plan, 3)
+            self._run(args)
+        level_start = self.level
+        self.level -= ITER_DEPTH
+        self.s_w = self.s_v = plan.s_out
+        self.alpha0, self.alpha1 = self.alpha1, next_alpha(self.alpha1)
+        self.t += 1
+        return dict(iteration=self.t, lr=lr, eta=eta, gamma=gamma, level_start=level_start,
+                    level_after=self.level, refreshed=refreshed)
+
+    # ------------------------------------------------------------ readout
+    def weights(self) -> np.ndarray:
+        """Decrypt W and read row 0 of each column block (decode_weights,
+        enctrain.py:266-289, without the exact replication check)."""
+        ctx, lay = self.ctx, self.layout
+        C = self.cols
+        out = torch.empty((C, self.ck.n), dtype=torch.int64, device=ctx.device)
+        ctx._call("helr_decrypt", ctx.sk.data_ptr(), self.wv.data_ptr(), C, self.level, out.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+        coef = out.cpu().numpy()
+        segs = []
+        for j in range(C):
+            grid = ctx.encoder.decode(coef[j], self.s_w).reshape(lay.m, lay.g)
+            segs.append(np.real(grid[0]))
+        return np.concatenate(segs)[: lay.cols]
+
+    def close(self):
+        if self._graph is not None:
+            self.lib.helr_nag_graph_destroy(self._graph)
+            self._graph = None
