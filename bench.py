@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py — encrypted enhanced-NAG logistic-regression training on B200.
+
+Metric (BASELINE.json): encrypted NAG iterations/s at the paper shape
+(422,108 x 200 padded to 256, N = 2^16, 1,024-row mini-batches packed as 8
+ciphertexts of 128 x 256), plus epoch time and HBM GB/s.  One "step" is one
+full NAG iteration over one batch: Z.W products, sum_col_vec, degree-3
+sigmoid complement, gradient, sum_rows, quadratic-gradient product, NAG
+update, and the refresh stand-in of W/V (every iteration at L = 8 primes).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload paper_mini]
+    python bench.py --impl reference ...   # the reference algorithm on host cores
+
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks; every step reads a different batch (64 MiB of
+ciphertexts) and streams 24 Galois keys (~830 MB), far beyond the 126 MB L2,
+so no flush is needed between steps.  Multi-GPU: independent replicas
+(the mini-batch path does not shard), scaling "weak".
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "encrypted NAG iterations/sec and epoch time at 422,108x200, N=2^16; HBM GB/s"
+UNIT = "iterations/s"
+CATS = ["ntt", "modup", "ks_inner", "moddown", "tensor", "rescale", "elementwise", "other"]
+
+WORKLOADS = {
+    # name: (dataset factory kwargs, log_n, L primes, dnum, rows per block, blocks per batch, mode)
+    "paper_mini": dict(data="paper", log_n=16, L=8, dnum=3, rows=128, blocks=8, mode="mini_batch"),
+    "paper_full": dict(data="paper", log_n=16, L=8, dnum=3, rows=128, blocks=8, mode="full_batch"),
+    "medium": dict(data="medium", log_n=15, L=8, dnum=3, rows=1024, blocks=1, mode="mini_batch"),
+    "toy": dict(data="toy", log_n=13, L=8, dnum=3, rows=128, blocks=1, mode="mini_batch"),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=None, help="timed iterations (default: one epoch)")
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=list(WORKLOADS), default="paper_mini")
+    p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-iters", type=int, default=200, help="bounded CPU-baseline sample (iterations)")
+    p.add_argument("--cpu-rns", action="store_true", help="also time the CPU RNS-CKKS oracle (1 iteration)")
+    p.add_argument("--profile-steps", type=int, default=4)
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_dataset(name):
+    from paper_2406_13221_b200 import data
+    return {"paper": data.paper_dataset, "medium": data.medium_dataset, "toy": data.toy_dataset}[name]()
+
+
+def lr_fn(t):
+    return 1.0 + 10.0 * math.exp(-t)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    path = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(path.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, if any."""
+    path = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(path.read_text())
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------- reference arm
+def cpu_reference_sample(wl, iters):
+    """The reference's own algorithm (slot-level simulator circuit, restated
+    in oracle/slotsim.py) on host cores, bounded to ``iters`` iterations."""
+    from oracle import slotsim
+    from paper_2406_13221_b200.optimizer import BASELINE_CUBIC
+    ds = make_dataset(wl["data"])
+    qpoly = BASELINE_CUBIC.complement().padded(3)
+    mode = wl["mode"]
+    if mode == "full_batch":
+        iters = max(1, min(iters, 2))
+    t0 = time.perf_counter()
+    slotsim.train(ds.X, ds.y, wl["log_n"], wl["rows"], wl["blocks"], qpoly, lr_fn, 0, mode=mode, trace=False)
+    t_prep = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    slotsim.train(ds.X, ds.y, wl["log_n"], wl["rows"], wl["blocks"], qpoly, lr_fn, iters, mode=mode, trace=False)
+    dt = time.perf_counter() - t0 - t_prep
+    return iters / dt, dt, iters
+
+
+def run_reference(args, wl, ws, rank):
+    if rank != 0:
+        return
+    steps = args.steps if args.steps is not None else 100
+    warm = max(0, args.warmup)
+    from oracle import slotsim  # noqa: F401
+    cores = 1  # numpy slot arithmetic is single-threaded
+    # warm-up + timed sample, each step one iteration of the reference circuit
+    rate, dt, iters = cpu_reference_sample(wl, steps + warm)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws, "steps": steps,
+        "warmup": warm, "ms_per_step": 1000.0 / rate, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "n": 422108 if "paper" in args.workload else None,
+                   "batch_rows": wl["rows"] * wl["blocks"], "log_n": wl["log_n"], "parallelism": "replicas"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{iters} iterations of the reference simulator circuit (oracle/slotsim.py)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "epoch_s": 413.0 / rate if "paper" in args.workload else None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl, ws, rank)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2406_13221_b200 import _lib
+    from paper_2406_13221_b200.ckks import GpuContext
+    from paper_2406_13221_b200.driver import FusedTrainer
+    from paper_2406_13221_b200.params import CkksParams
+
+    lib = _lib.load()
+    lib.helr_prof_collect.argtypes = [ctypes.POINTER(ctypes.c_double)] * 2 + [ctypes.POINTER(ctypes.c_int)]
+    lib.helr_prof_enable.argtypes = [ctypes.c_int]
+    lib.helr_launch_count.restype = ctypes.c_ulonglong
+
+    t_setup = time.perf_counter()
+    ck = CkksParams.generate(log_n=wl["log_n"], n_q=wl["L"], dnum=wl["dnum"])
+    ctx = GpuContext(ck, seed=1, max_batch=max(8, wl["blocks"]))
+    ds = make_dataset(wl["data"])
+    tr = FusedTrainer(ctx, ds, rows_per_block=wl["rows"], blocks_per_batch=wl["blocks"], mode=wl["mode"],
+                      use_graph=not args.no_graph)
+    setup_s = time.perf_counter() - t_setup
+    steps = args.steps if args.steps is not None else tr.n_batches
+    warm = max(3, args.warmup)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    stream = tr.stream  # all trainer work (and these events) live on its stream
+    for _ in range(warm):
+        tr.iterate()
+    barrier()
+
+    # ---------------- timed region: device-resident dataset
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        tr.iterate()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = steps * ws / (ms / 1000.0)
+
+    # ---------------- live per-kernel attribution (eager launches, CUDA events)
+    tr_graph = tr.use_graph
+    tr.use_graph = False
+    c0 = lib.helr_launch_count()
+    lib.helr_prof_enable(1)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    for _ in range(args.profile_steps):
+        tr.iterate()
+    pe1.record(stream)
+    lib.helr_prof_enable(0)
+    msa = (ctypes.c_double * 8)()
+    bya = (ctypes.c_double * 8)()
+    cna = (ctypes.c_int * 8)()
+    lib.helr_prof_collect(msa, bya, cna)
+    launches_per_step = (lib.helr_launch_count() - c0) / args.profile_steps
+    prof_ms = pe0.elapsed_time(pe1)
+    tr.use_graph = tr_graph
+    cats = {CATS[i]: {"ms": msa[i] / args.profile_steps, "launches": cna[i] / args.profile_steps,
+                      "gb": bya[i] / args.profile_steps / 1e9} for i in range(8)}
+    dom = max(range(8), key=lambda i: msa[i])
+    peak, peak_kind = peaks()
+    achieved = (bya[dom] / cna[dom]) / ((msa[dom] / cna[dom]) / 1000.0) / 1e9
+    traffic = ncu_traffic().get(CATS[dom])
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": CATS[dom], "peak_kind": peak_kind,
+                "share_of_step": msa[dom] / prof_ms,
+                "algorithmic_bytes_per_launch": bya[dom] / cna[dom],
+                "avg_launch_ms": msa[dom] / cna[dom]}
+    step_gb = sum(bya) / args.profile_steps / 1e9
+
+    # ---------------- e2e: host-resident encrypted dataset through the public API
+    e2e = None
+    if not args.no_e2e:
+        tr.enable_host_stream()
+        for _ in range(2):
+            tr.iterate()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(steps):
+            tr.iterate()
+        f1.record(stream)
+        barrier()
+        ems = f0.elapsed_time(f1)
+        if ws > 1:
+            t = torch.tensor([ems], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d, d2h = tr.bytes_per_step()
+        e2e = {"value": steps * ws / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / steps}
+        tr.disable_host_stream()
+
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and args.cpu_iters > 0:
+        rate, dt, iters = cpu_reference_sample(wl, args.cpu_iters)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{iters} iterations of the reference simulator circuit (oracle/slotsim.py), {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps, "warmup": warm,
+            "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic",
+            "config": {"workload": args.workload, "n": ds.n_samples, "features": ds.n_features,
+                       "padded_cols": tr.layout.col_blocks * tr.layout.g, "log_n": ck.log_n, "L": ck.L,
+                       "K": ck.K, "dnum": ck.dnum, "batch_rows": tr.batch_rows, "cts_per_batch": tr.rows,
+                       "batches": tr.n_batches, "mode": wl["mode"], "parallelism": "replicas",
+                       "cuda_graph": tr.use_graph,
+                       "l2": "no flush needed: each step streams a new 64 MiB batch and ~830 MB of keys"},
+            "epoch_s": tr.n_batches / (value / ws),
+            "hbm_gbs_step": step_gb / (ms / steps / 1000.0),
+            "algorithmic_gb_per_step": step_gb,
+            "roofline": roofline,
+            "kernels": cats,
+            "gpu_launches": int(round(launches_per_step * steps)),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "setup_s": setup_s,
+            "prepare_s": tr.timings.get("prepare_s"),
+        }
+        print(json.dumps(line), flush=True)
+    tr.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -184,6 +184,17 @@ int helr_nag_graph_capture(helr_ctx* ctx, const helr_nag_args* args, void* strea
 int helr_nag_graph_launch(void* graph_exec, void* stream);
 int helr_nag_graph_destroy(void* graph_exec);
 
+/* ---- instrumentation (not part of the reference surface) ---------------- */
+
+/* Per-launch CUDA-event timing by kernel category (0 NTT, 1 ModUp, 2 key
+ * inner product, 3 ModDown, 4 tensor, 5 rescale, 6 elementwise, 7 other);
+ * bytes are the algorithmic bytes each launch must move. */
+#define HELR_PROF_NCAT 8
+int helr_prof_enable(int on);
+int helr_prof_collect(double* ms, double* bytes, int* launches);
+/* Running count of kernels this library has launched (eager launches). */
+unsigned long long helr_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -444,6 +444,53 @@ void oc_basis_convert(oc_ctx* c, const u64* in, const int* src, int ns, u64* out
     }
 }
 
+/* Centred P -> Q_l conversion for ModDown: the CENTRED representative
+ * a_c in (-P/2, P/2] of the integer a given by its residues mod p_k (coefficient
+ * form), reduced mod q_i.  With y_k = [a_k (P/p_k)^-1]_{p_k},
+ * a = sum_k y_k P/p_k - r P where r = round(sum_k y_k / p_k); r is computed
+ * in IEEE double (no FMA: y_k * (1/p_k) then a running sum in k order, then
+ * floor(v + 0.5)), exactly as the device does, so both round identically.
+ * Removing the [0, K) overflow bias of the plain fast conversion keeps the
+ * key-switching error zero-mean (a biased error times the secret key
+ * concentrates ~1e-7 on the slots next to zeta^{+-1}). */
+void oc_moddown_convert(oc_ctx* c, const u64* in, u64* out, int nl) {
+    int N = c->n, L = c->L, K = c->K;
+    u64 hinv[MAXP];
+    double pinv[MAXP];
+    for (int k = 0; k < K; k++) {
+        u64 pk = c->prm[L + k], prod = 1;
+        for (int k2 = 0; k2 < K; k2++)
+            if (k2 != k) prod = mulm(prod, c->prm[L + k2] % pk, pk);
+        hinv[k] = invm(prod, pk);
+        pinv[k] = 1.0 / (double)pk;
+    }
+    for (int i = 0; i < nl; i++) {
+        u64 q = c->prm[i];
+        u64 hmod[MAXP], pm = 1;
+        for (int k = 0; k < K; k++) {
+            u64 prod = 1;
+            for (int k2 = 0; k2 < K; k2++)
+                if (k2 != k) prod = mulm(prod, c->prm[L + k2] % q, q);
+            hmod[k] = prod;
+            pm = mulm(pm, c->prm[L + k] % q, q);
+        }
+        u64* o = out + (size_t)i * N;
+        for (int n = 0; n < N; n++) {
+            u64 acc = 0;
+            volatile double v = 0.0;
+            for (int k = 0; k < K; k++) {
+                u64 y = mulm(in[(size_t)k * N + n], hinv[k], c->prm[L + k]);
+                volatile double t = (double)y * pinv[k];
+                v = v + t;
+                acc = addm(acc, mulm(y % q, hmod[k], q), q);
+            }
+            volatile double vh = v + 0.5;
+            u64 r = (u64)floor(vh);
+            o[n] = subm(acc, mulm(r % q, pm, q), q);
+        }
+    }
+}
+
 /* ---------------- key switching ----------------
  * d: NTT-form limbs 0..level of one polynomial (limb stride N).
  * evk: u64[beta][2][L+K][N].  k0, k1: outputs, limbs 0..level (stride N). */
@@ -495,16 +542,13 @@ void oc_keyswitch(oc_ctx* c, const u64* d, const u64* evk, int level, u64* k0, u
     free(up);
     free(coef);
     /* ModDown */
-    int srcP[MAXP], dstQ[MAXP];
-    for (int k = 0; k < K; k++) srcP[k] = L + k;
-    for (int i = 0; i < nl; i++) dstQ[i] = i;
     u64* pc = (u64*)malloc(sizeof(u64) * (size_t)K * N);
     u64* conv = (u64*)malloc(sizeof(u64) * (size_t)nl * N);
     for (int b = 0; b < 2; b++) {
         u64* a = acc + (size_t)b * ext * N;
         memcpy(pc, a + (size_t)nl * N, sizeof(u64) * (size_t)K * N);
         for (int k = 0; k < K; k++) oc_intt(c, pc + (size_t)k * N, L + k);
-        oc_basis_convert(c, pc, srcP, K, conv, dstQ, nl);
+        oc_moddown_convert(c, pc, conv, nl);
         u64* outp = b == 0 ? k0 : k1;
         for (int i = 0; i < nl; i++) {
             u64 q = c->prm[i];

@@ -159,7 +159,7 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
         }
     // ModDown constants
     size_t o_phi = put(K), o_phis = put(K), o_phm = put((size_t)K * L), o_phms = put((size_t)K * L);
-    size_t o_pi = put(L), o_pis = put(L), o_pm = put(L);
+    size_t o_pi = put(L), o_pis = put(L), o_pm = put(L), o_pms = put(L), o_pid = put(K);
     for (int k = 0; k < K; k++) {
         u64 pk = primes[L + k], prod = 1;
         for (int k2 = 0; k2 < K; k2++)
@@ -178,8 +178,13 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
         u64 qi = primes[i], pm = 1;
         for (int k = 0; k < K; k++) pm = hmul(pm, primes[L + k] % qi, qi);
         h[o_pm + i] = pm;
+        h[o_pms + i] = hshoup(pm, qi);
         h[o_pi + i] = hinv(pm, qi);
         h[o_pis + i] = hshoup(h[o_pi + i], qi);
+    }
+    for (int k = 0; k < K; k++) {  // 1/p_k as IEEE double bits (centred ModDown)
+        double inv = 1.0 / (double)primes[L + k];
+        memcpy(&h[o_pid + k], &inv, sizeof(double));
     }
     // X^(N/2) in NTT form per ciphertext prime (imul)
     size_t o_im = put((size_t)L * n);
@@ -212,7 +217,7 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
     c->qlinv = d + o_ql; c->qlinv_sh = d + o_qls;
     c->md_phinv = d + o_phi; c->md_phinv_sh = d + o_phis;
     c->md_phmod = d + o_phm; c->md_phmod_sh = d + o_phms;
-    c->md_pinv = d + o_pi; c->md_pinv_sh = d + o_pis; c->pmod = d + o_pm;
+    c->md_pinv = d + o_pi; c->md_pinv_sh = d + o_pis; c->pmod = d + o_pm; c->pmod_sh = d + o_pms; c->md_pinv_dbl = d + o_pid;
     c->imul_f = d + o_im;
     c->modup = d;  // offsets in modup_off are absolute word offsets into d_tab
 

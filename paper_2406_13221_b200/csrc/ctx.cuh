@@ -55,6 +55,8 @@ struct helr_ctx {
     const u64* md_pinv = nullptr;      // [L] P^-1 mod q_i
     const u64* md_pinv_sh = nullptr;
     const u64* pmod = nullptr;         // [L] P mod q_i
+    const u64* pmod_sh = nullptr;
+    const u64* md_pinv_dbl = nullptr;  // [K] bits of (double)1/p_k
     const u64* imul_f = nullptr;       // [L][N] NTT of X^(N/2)
     // key-switching workspace
     u64* ws = nullptr;

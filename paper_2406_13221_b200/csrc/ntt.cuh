@@ -20,6 +20,9 @@
 // instead of making extra passes over HBM.
 #pragma once
 #include "ctx.cuh"
+#include "prof.cuh"
+
+void count_launches(int k);
 
 struct NttPassArgs {
     int log_n;
@@ -198,6 +201,7 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
     NttPassArgs a{log_n, st0, final_out};
     dim3 grid(subs / cols, map.count, count);
     const int threads = T * cols / (1 << LOG_R);
+    count_launches(1);
     if (cols == COLS) {
         ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV><<<grid, threads, 0, s>>>(ld, st, tb, map, a);
     } else {
@@ -247,6 +251,7 @@ template <bool INV, class Ld, class St>
 static void ntt_launch(const helr_ctx* c, const Ld& ld, const St& st, u64* mid, long long mid_stride,
                        const LimbMap& map, int count, cudaStream_t s) {
     const int log_n = c->log_n;
+    ProfScope ps(PROF_NTT, 16.0 * c->n * map.count * count, s);
     if (log_n <= 11) {
         ntt_single<INV>(log_n, ld, st, c->t, map, count, s);
         return;

@@ -17,9 +17,16 @@
 #include "../../include/helr_ckks.h"
 #include "ntt.cuh"
 #include "ops_internal.cuh"
+#include "prof.cuh"
 
 #define CHECK_LAUNCH(what)                                              \
     do {                                                                \
+        if (!cuda_ok(cudaGetLastError(), what)) return HELR_ECUDA;      \
+    } while (0)
+// one non-NTT kernel launched (NTT passes count themselves in ntt.cuh)
+#define CHECK_KERNEL(what)                                              \
+    do {                                                                \
+        count_launches(1);                                              \
         if (!cuda_ok(cudaGetLastError(), what)) return HELR_ECUDA;      \
     } while (0)
 
@@ -83,8 +90,9 @@ int op_ew(helr_ctx* c, int op, const u64* a, long long as, const u64* b, long lo
     long long total = (long long)count * 2 * (level + 1) * c->n;
     int blocks = blocks_for(total, 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
+    ProfScope ps(PROF_ELEM, 8.0 * total * ((op == EW_ADD || op == EW_SUB) ? 3 : 2), s);
     k_elementwise<<<blocks, 256, 0, s>>>(op, a, b, out, g, total, c->t, c->imul_f);
-    CHECK_LAUNCH("elementwise");
+    CHECK_KERNEL("elementwise");
     return HELR_OK;
 }
 
@@ -148,7 +156,7 @@ __global__ void k_fill_secret(u64* sk, int n, int LK, u64 seed, Tables tb) {
 
 extern "C" int helr_keygen_secret(helr_ctx* c, uint64_t* sk, uint64_t seed, void* s) {
     k_fill_secret<<<blocks_for(c->n, 256), 256, 0, S(s)>>>((u64*)sk, c->n, c->LK, seed, c->t);
-    CHECK_LAUNCH("keygen_secret");
+    CHECK_KERNEL("keygen_secret");
     LimbMap m = limb_range(0, c->LK);
     ntt_buffers<false>(c, (const u64*)sk, 0, (u64*)sk, 0, m, 1, S(s));
     CHECK_LAUNCH("keygen_secret ntt");
@@ -196,7 +204,7 @@ extern "C" int helr_keygen_switch(helr_ctx* c, const uint64_t* sk, int64_t galoi
     galois = galois % (2ll * c->n);
     dim3 g1(blocks_for(c->n, 256), c->beta);
     k_fill_key_error<<<g1, 256, 0, S(s)>>>((u64*)evk, c->n, c->LK, c->beta, seed, key_id, c->eta, c->t);
-    CHECK_LAUNCH("keygen error");
+    CHECK_KERNEL("keygen error");
     LimbMap m = limb_range(0, c->LK);
     const long long st = 2ll * c->LK * c->n;
     ntt_buffers<false>(c, (const u64*)evk, st, (u64*)evk, st, m, c->beta, S(s));
@@ -204,7 +212,7 @@ extern "C" int helr_keygen_switch(helr_ctx* c, const uint64_t* sk, int64_t galoi
     dim3 g2(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, c->LK, c->beta);
     k_key_combine<<<g2, 256, 0, S(s)>>>((u64*)evk, (const u64*)sk, c->n, c->log_n, c->L, c->LK, c->alpha, seed, key_id,
                                         (long long)galois, c->t, c->pmod);
-    CHECK_LAUNCH("keygen combine");
+    CHECK_KERNEL("keygen combine");
     return HELR_OK;
 }
 
@@ -238,14 +246,14 @@ static int encrypt_dev(helr_ctx* c, const u64* sk, const long long* msg, u64* ct
                        u64 first_id, cudaStream_t s) {
     dim3 g1(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
     k_enc_fill<<<g1, 256, 0, s>>>(ct, msg, c->n, c->L, level + 1, seed, first_id, c->eta, c->t);
-    CHECK_LAUNCH("encrypt fill");
+    CHECK_KERNEL("encrypt fill");
     LimbMap m = limb_range(0, level + 1);
     const long long st = 2ll * c->L * c->n;
     ntt_buffers<false>(c, ct, st, ct, st, m, count, s);
     CHECK_LAUNCH("encrypt ntt");
     dim3 g2(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, count);
     k_enc_combine<<<g2, 256, 0, s>>>(ct, sk, c->n, c->L, seed, first_id, c->t);
-    CHECK_LAUNCH("encrypt combine");
+    CHECK_KERNEL("encrypt combine");
     return HELR_OK;
 }
 
@@ -279,13 +287,13 @@ static int decrypt_dev(helr_ctx* c, const u64* sk, const u64* ct, int count, lon
                        u64* tmp, cudaStream_t s) {
     dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
     k_dec_combine<<<g, 256, 0, s>>>(ct, sk, tmp, c->n, c->L, c->t);
-    CHECK_LAUNCH("decrypt combine");
+    CHECK_KERNEL("decrypt combine");
     LimbMap m = limb_range(0, 1);
     ntt_buffers<true>(c, tmp, c->n, tmp, c->n, m, count, s);
     CHECK_LAUNCH("decrypt intt");
     long long total = (long long)count * c->n;
     k_center<<<blocks_for(total, 256) < 4096 ? blocks_for(total, 256) : 4096, 256, 0, s>>>(tmp, out, total, ratio, c->t);
-    CHECK_LAUNCH("decrypt center");
+    CHECK_KERNEL("decrypt center");
     return HELR_OK;
 }
 
@@ -313,7 +321,7 @@ extern "C" int helr_encode_plain(helr_ctx* c, const int64_t* msg, uint64_t* pt, 
     if (count < 1) return HELR_OK;
     dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
     k_plain_fill<<<g, 256, 0, S(s)>>>((const long long*)msg, (u64*)pt, c->n, c->L, level + 1, c->t);
-    CHECK_LAUNCH("plain fill");
+    CHECK_KERNEL("plain fill");
     LimbMap m = limb_range(0, level + 1);
     const long long st = (long long)c->L * c->n;
     ntt_buffers<false>(c, (const u64*)pt, st, (u64*)pt, st, m, count, S(s));
@@ -390,14 +398,20 @@ static int rescale_dev(helr_ctx* c, const u64* a, long long as, u64* out, long l
         CHECK_LAUNCH("rescale intt");
     }
     dim3 g1(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, items);
-    k_rescale_conv<<<g1, 256, 0, s>>>(r, t, n, l, c->t);
-    CHECK_LAUNCH("rescale conv");
+    {
+        ProfScope ps(PROF_RESCALE, 8.0 * n * items * (1 + l), s);
+        k_rescale_conv<<<g1, 256, 0, s>>>(r, t, n, l, c->t);
+        CHECK_KERNEL("rescale conv");
+    }
     LimbMap m = limb_range(0, l);
     ntt_buffers<false>(c, t, (long long)l * n, t, (long long)l * n, m, items, s);
     CHECK_LAUNCH("rescale ntt");
     dim3 g2(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, l, items);
-    k_rescale_final<<<g2, 256, 0, s>>>(a, as, t, out, os, n, L, l, c->qlinv, c->qlinv_sh, c->t);
-    CHECK_LAUNCH("rescale final");
+    {
+        ProfScope ps(PROF_RESCALE, 8.0 * n * items * l * 3, s);
+        k_rescale_final<<<g2, 256, 0, s>>>(a, as, t, out, os, n, L, l, c->qlinv, c->qlinv_sh, c->t);
+        CHECK_KERNEL("rescale final");
+    }
     return HELR_OK;
 }
 
@@ -532,9 +546,12 @@ __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long 
 }
 
 // ModDown conversion: mdc[b][poly][i] = sum_k [a_k * phinv_k]_{p_k} * phmod[k][i] mod q_i
+// Centred conversion (see oracle oc_moddown_convert): subtract r*P with
+// r = round(sum_k y_k / p_k) evaluated in IEEE double without contraction,
+// so the ModDown error is the zero-mean rounding of x / P.
 __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n,
                                int nl, int K, int L, const u64* phinv, const u64* phinv_sh, const u64* phm,
-                               const u64* phms, Tables tb) {
+                               const u64* phms, const u64* pinv_dbl, const u64* pm, const u64* pm_sh, Tables tb) {
     const int it = blockIdx.y;  // item*2 + poly
     const int b = it >> 1, poly = it & 1;
     const int ne = nl + K;
@@ -542,16 +559,19 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
     u64* mp = mdc + (size_t)b * mdc_item_stride + (size_t)poly * L * n;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         u64 z[HELR_MAXP];
+        double v = 0.0;
         for (int k = 0; k < K; k++) {
             const u64 pk = tb.q[L + k];
             z[k] = shoup(ap[(size_t)(nl + k) * n + i], phinv[k], phinv_sh[k], pk);
+            v = __dadd_rn(v, __dmul_rn(__ull2double_rn(z[k]), __longlong_as_double((long long)pinv_dbl[k])));
         }
+        const u64 r = (u64)__double2ull_rd(__dadd_rn(v, 0.5));
         for (int p = 0; p < nl; p++) {
             const u64 q = tb.q[p];
             u64 s = 0;
             for (int k = 0; k < K; k++)
                 s = add_mod(s, shoup(z[k], phm[(size_t)k * L + p], phms[(size_t)k * L + p], q), q);
-            mp[(size_t)p * n + i] = s;
+            mp[(size_t)p * n + i] = sub_mod(s, shoup(r, pm[p], pm_sh[p], q), q);
         }
     }
 }
@@ -630,8 +650,9 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
         ModUpArgs a{w.coef, w.coef_s, in.d, in.d_stride, in.galois, w.ext, w.ext_s, w.ext_ds, c->d_tab, c->d_modup_offs + (size_t)level * c->beta,
                     n, c->log_n, nl, K, L, c->alpha};
         dim3 g(blocks_for(n, 128) < 64 ? blocks_for(n, 128) : 64, nd, B);
+        ProfScope ps(PROF_MODUP, 8.0 * n * B * (2.0 * nl + (double)nd * ne), s);
         k_modup<<<g, 128, 0, s>>>(a, c->t);
-        CHECK_LAUNCH("ks modup");
+        CHECK_KERNEL("ks modup");
     }
     // 3) NTT of the converted limbs, per digit
     for (int j = 0; j < nd; j++) {
@@ -651,8 +672,9 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
     // 4) inner product with the key
     {
         dim3 g(blocks_for(n, 256) < 32 ? blocks_for(n, 256) : 32, ne);
+        ProfScope ps(PROF_INNER, 8.0 * n * ((double)B * nd * ne + 2.0 * nd * ne + 2.0 * B * ne), s);
         k_ks_inner<4><<<g, 256, 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B, c->t);
-        CHECK_LAUNCH("ks inner");
+        CHECK_KERNEL("ks inner");
     }
     // 5) ModDown: INTT of the P limbs (both polys), conversion, NTT, combine
     {
@@ -667,9 +689,12 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
         }
         CHECK_LAUNCH("ks moddown intt");
         dim3 g(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, 2 * B);
-        k_moddown_conv<<<g, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv, c->md_phinv_sh,
-                                         c->md_phmod, c->md_phmod_sh, c->t);
-        CHECK_LAUNCH("ks moddown conv");
+        {
+            ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + nl), s);
+            k_moddown_conv<<<g, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv, c->md_phinv_sh,
+                                             c->md_phmod, c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
+            CHECK_KERNEL("ks moddown conv");
+        }
         LimbMap mq = limb_range(0, nl);
         for (int poly = 0; poly < 2; poly++) {
             u64* base = w.mdc + (size_t)poly * L * n;
@@ -677,9 +702,12 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
         }
         CHECK_LAUNCH("ks moddown ntt");
         dim3 g2(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, nl, 2 * B);
-        k_moddown_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, ep, n, c->log_n, nl, K, L, c->md_pinv,
-                                           c->md_pinv_sh, c->t);
-        CHECK_LAUNCH("ks moddown final");
+        {
+            ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * nl * (3.0 + (ep.add_a ? 1 : 0) + (ep.add_p ? 0.5 : 0)), s);
+            k_moddown_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, ep, n, c->log_n, nl, K, L, c->md_pinv,
+                                               c->md_pinv_sh, c->t);
+            CHECK_KERNEL("ks moddown final");
+        }
     }
     return HELR_OK;
 }
@@ -729,8 +757,11 @@ int op_mul_relin_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, 
         KsWs w = ks_ws(c, chunk);
         dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, nb);
         TensorArgs ta{a + (size_t)b0 * a_is, a_is, a_ts, b + (size_t)b0 * b_is, b_is, b_ts, terms};
-        k_tensor<<<g, 256, 0, s>>>(ta, w.tensor, c->n, c->L, c->t);
-        CHECK_LAUNCH("tensor");
+        {
+            ProfScope ps(PROF_TENSOR, 8.0 * c->n * nb * (level + 1) * (4.0 * terms + 3.0), s);
+            k_tensor<<<g, 256, 0, s>>>(ta, w.tensor, c->n, c->L, c->t);
+            CHECK_KERNEL("tensor");
+        }
         const long long ts = 3ll * c->L * c->n;
         KsInput in{w.tensor + 2ll * c->L * c->n, ts, 0};
         KsEpilogue ep{out + (size_t)b0 * os, os, w.tensor, ts, nullptr, 0, 0};
@@ -804,7 +835,8 @@ int op_lincomb(helr_ctx* c, int terms, const u64* const* x, const long long* xs,
     }
     la.terms = terms;
     dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, 2 * count);
+    ProfScope ps(PROF_ELEM, 8.0 * c->n * 2.0 * count * (level + 1) * (terms + 1), s);
     k_lincomb<<<g, 256, 0, s>>>(la, out, os, c->n, c->L, c->t);
-    CHECK_LAUNCH("lincomb");
+    CHECK_KERNEL("lincomb");
     return HELR_OK;
 }

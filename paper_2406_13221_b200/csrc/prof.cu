@@ -1,0 +1,71 @@
+// prof.cu — event-pair recorder behind prof.cuh and its C ABI.
+#include <vector>
+
+#include "../../include/helr_ckks.h"
+#include "ctx.cuh"
+#include "prof.cuh"
+
+namespace {
+struct Rec {
+    int cat;
+    double bytes;
+    cudaEvent_t a, b;
+};
+bool g_on = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+int g_open = -1;
+
+cudaEvent_t take() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+bool prof_enabled() { return g_on; }
+
+static unsigned long long g_launches = 0;
+void count_launches(int k) { g_launches += (unsigned long long)k; }
+extern "C" unsigned long long helr_launch_count(void) { return g_launches; }
+
+void prof_begin(int cat, double bytes, cudaStream_t s) {
+    Rec r{cat, bytes, take(), take()};
+    cudaEventRecord(r.a, s);
+    g_recs.push_back(r);
+    g_open = (int)g_recs.size() - 1;
+}
+
+void prof_end(cudaStream_t s) {
+    if (g_open < 0) return;
+    cudaEventRecord(g_recs[g_open].b, s);
+    g_open = -1;
+}
+
+extern "C" int helr_prof_enable(int on) {
+    g_on = on != 0;
+    return HELR_OK;
+}
+
+// Synchronises, then fills per-category totals: ms[cat], bytes[cat],
+// launches[cat] (arrays of HELR_PROF_NCAT) and clears the record list.
+extern "C" int helr_prof_collect(double* ms, double* bytes, int* launches) {
+    if (!cuda_ok(cudaDeviceSynchronize(), "prof sync")) return HELR_ECUDA;
+    for (int c = 0; c < PROF_NCAT; c++) { ms[c] = 0; bytes[c] = 0; launches[c] = 0; }
+    for (auto& r : g_recs) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        ms[r.cat] += t;
+        bytes[r.cat] += r.bytes;
+        launches[r.cat] += 1;
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+    return HELR_OK;
+}

@@ -142,12 +142,16 @@ class FusedTrainer:
     blocks cover the f+1 coefficients.  Mini-batch mode visits one batch
     per iteration in order; full-batch mode sums every batch's gradient
     before one B̄ product and update (enctrain.py:356-359, 374-381).
+
+    Every iteration reads its batch from fixed staging buffers (filled by a
+    device-to-device copy from the HBM-resident encrypted dataset, or by a
+    host-to-device copy when ``host_stream`` is set), so one captured CUDA
+    graph per phase serves every batch.
     """
 
     def __init__(self, ctx: GpuContext, ds, rows_per_block: int, blocks_per_batch: int = 1,
                  mode: str = "mini_batch", poly: PolyApprox = BASELINE_CUBIC, schedule=None,
-                 epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False,
-                 z_on_host: bool = False):
+                 epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False):
         if mode not in ("mini_batch", "full_batch"):
             raise ValueError(f"mode must be mini_batch or full_batch, got {mode!r}")
         from .optimizer import ExpDecay
@@ -171,10 +175,14 @@ class FusedTrainer:
         self.qpoly = poly.complement().padded(3)
         self.lib = _lib.load()
         _bind(self.lib)
-        self._graph = None
-        self._graph_key = None
+        self._graphs: dict = {}
+        self._warm = False
+        # graph capture is not allowed on the legacy default stream
+        self.stream = torch.cuda.Stream(device=ctx.device)
         self.timings: dict = {}
-        self.z_on_host = z_on_host
+        self.host_stream = False
+        self.z_host = None
+        self.b_host = None
         self._prepare()
 
     # ------------------------------------------------------------ client side
@@ -184,49 +192,41 @@ class FusedTrainer:
         Z = ds.X * ds.y[:, None]
         blocks = pack_matrix_array(Z, lay)                       # (row_blocks, cols, S)
         nb, R, C = self.n_batches, self.rows, self.cols
-        full = np.zeros((nb * R, C, ck.slots))
-        full[: lay.row_blocks] = blocks
         top = ck.top_level
         s_top = ck.level_scales[top]
         L, N = ck.L, ck.n
-        store_dev = "cpu" if self.z_on_host else ctx.device
-        self.z = torch.empty((nb, R, C, 2, L, N), dtype=torch.int64, device=store_dev,
-                             pin_memory=bool(self.z_on_host))
-        chunk = 64
-        flat = full.reshape(nb * R * C, ck.slots)
+        self.z = torch.empty((nb, R, C, 2, L, N), dtype=torch.int64, device=ctx.device)
         zflat = self.z.view(nb * R * C, 2, L, N)
-        stage = None if not self.z_on_host else torch.empty((chunk, 2, L, N), dtype=torch.int64, device=ctx.device)
-        for s in range(0, flat.shape[0], chunk):
+        nblk = lay.row_blocks * C
+        flat = blocks.reshape(nblk, ck.slots)
+        chunk = 64
+        for s in range(0, nblk, chunk):
             coef = ctx.encoder.encode(flat[s:s + chunk], s_top)
-            if self.z_on_host:
-                ctx.encrypt_to(coef, stage[: coef.shape[0]], top)
-                zflat[s:s + coef.shape[0]].copy_(stage[: coef.shape[0]])
-            else:
-                ctx.encrypt_to(coef, zflat[s:s + coef.shape[0]], top)
+            ctx.encrypt_to(coef, zflat[s:s + coef.shape[0]], top)
+        if nb * R * C > nblk:  # zero blocks padding the last batch (encryptions of 0)
+            pad = nb * R * C - nblk
+            ctx.encrypt_to(np.zeros((pad, N), dtype=np.int64), zflat[nblk:], top)
         self.s_z = s_top
-        # B̄: one per batch (mini) or merged over batches (full); computed on
-        # the real rows of each batch (enctrain.py:132-142, BASELINE "per batch")
-        scalers = []
+        # B̄ per batch (mini) or merged over batches (full), from the real rows
+        # of each batch (enctrain.py:132-142; BASELINE: "computed per batch")
+        self.scalers = []
         for b in range(nb):
             lo = b * self.batch_rows
             hi = min(lo + self.batch_rows, ds.n_samples)
-            scalers.append(scaler_for(ds.X[lo:hi], self.epsilon))
-        self.scalers = scalers
-        if self.mode == "full_batch":
-            vecs = [merge_bbar(scalers).b]
-        else:
-            vecs = [s.b for s in scalers]
+            self.scalers.append(scaler_for(ds.X[lo:hi], self.epsilon))
+        vecs = [merge_bbar(self.scalers).b] if self.mode == "full_batch" else [s.b for s in self.scalers]
         bb = np.stack([np.stack(replicate_rows(v, lay)) for v in vecs])   # (nbb, C, S)
         self.bbar = torch.empty((bb.shape[0], C, 2, L, N), dtype=torch.int64, device=ctx.device)
         bflat = bb.reshape(-1, ck.slots)
-        out = self.bbar.view(-1, 2, L, N)
+        bout = self.bbar.view(-1, 2, L, N)
         for s in range(0, bflat.shape[0], chunk):
             coef = ctx.encoder.encode(bflat[s:s + chunk], s_top)
-            ctx.encrypt_to(coef, out[s:s + coef.shape[0]], top)
+            ctx.encrypt_to(coef, bout[s:s + coef.shape[0]], top)
         self.s_b = s_top
         # W0 = V0 = enc(0) at the top level (enctrain.py:145-151)
         self.wv = torch.empty((2 * C, 2, L, N), dtype=torch.int64, device=ctx.device)
         ctx.encrypt_to(np.zeros((2 * C, N), dtype=np.int64), self.wv, top)
+        self.wv_tmp = torch.empty_like(self.wv)
         self.level = top
         self.s_w = self.s_v = s_top
         self.alpha0 = ALPHA0_INIT
@@ -241,13 +241,38 @@ class FusedTrainer:
         self._k_left, self._k_right, self._k_rows = keys(self.gal_left), keys(self.gal_right), keys(self.gal_rows)
         self._masks: dict = {}
         self.consts_dev = torch.zeros((NCONST, L), dtype=torch.int64, device=ctx.device)
-        self.consts_host = torch.zeros((NCONST, L), dtype=torch.int64, pin_memory=True)
+        self.consts_host = torch.zeros((NCONST, L), dtype=torch.int64).pin_memory()
         self.grad = torch.empty((C, 2, L, N), dtype=torch.int64, device=ctx.device)
-        self.zstage = None
-        if self.z_on_host:
-            self.zstage = torch.empty((R, C, 2, L, N), dtype=torch.int64, device=ctx.device)
+        self.zstage = torch.empty((R, C, 2, L, N), dtype=torch.int64, device=ctx.device)
+        self.bstage = torch.empty((C, 2, L, N), dtype=torch.int64, device=ctx.device)
+        self.w_host = torch.empty((2 * C, 2, L, N), dtype=torch.int64).pin_memory()
         torch.cuda.synchronize()
         self.timings["prepare_s"] = time.perf_counter() - t0
+
+    def enable_host_stream(self):
+        """Keep the encrypted dataset in pinned host memory and stream each
+        batch to the device inside the iteration (the e2e path)."""
+        if self.z_host is None:
+            self.z_host = torch.empty(self.z.shape, dtype=torch.int64, pin_memory=True)
+            self.z_host.copy_(self.z)
+            self.b_host = torch.empty(self.bbar.shape, dtype=torch.int64, pin_memory=True)
+            self.b_host.copy_(self.bbar)
+        self.host_stream = True
+
+    def disable_host_stream(self):
+        self.host_stream = False
+
+    def bytes_per_step(self) -> tuple:
+        """(H2D, D2H) bytes a host-streamed mini-batch step moves."""
+        cs = self.wv[0].numel() * 8
+        h2d = (self.rows * self.cols + self.cols) * cs + NCONST * self.ck.L * 8
+        active = (self.level_after_next() + 1) * self.ck.n * 8 * 2
+        d2h = 2 * self.cols * active
+        return h2d, d2h
+
+    def level_after_next(self) -> int:
+        lvl = self.level if self.level >= ITER_DEPTH else self.ck.top_level
+        return lvl - ITER_DEPTH
 
     def _mask(self, lw: int, scale: float) -> torch.Tensor:
         key = (lw, round(scale))
@@ -274,25 +299,24 @@ class FusedTrainer:
         return True
 
     def refresh(self):
+        """Refresh stand-in on W and V (NOT bootstrapping; see helr_refresh)."""
         ck = self.ck
         top = ck.top_level
         ratio = ck.level_scales[top] / self.s_w
-        out = torch.empty_like(self.wv)
         first = self.ctx._take_ct_ids(self.wv.shape[0])
+        stream = torch.cuda.current_stream().cuda_stream
         self.ctx._call("helr_refresh", self.ctx.sk.data_ptr(), self.wv.data_ptr(), self.level, float(ratio),
-                       out.data_ptr(), top, self.wv.shape[0], self.ctx.enc_seed, first,
-                       torch.cuda.current_stream().cuda_stream)
-        self.wv = out
+                       self.wv_tmp.data_ptr(), top, self.wv.shape[0], self.ctx.enc_seed, first, stream)
+        self.wv.copy_(self.wv_tmp)
         self.level = top
         self.s_w = self.s_v = ck.level_scales[top]
-        self._graph_key = None  # pointers changed
 
-    def _args(self, z_ptr: int, bbar_ptr: int, plan: IterPlan, phase: int) -> NagArgs:
+    def _args(self, plan: IterPlan, phase: int) -> NagArgs:
         C = self.cols
         cs = self.wv[0].numel() * 8
-        return NagArgs(z=z_ptr, rows=self.rows, cols=C, log_g=self.log_g, log_m=self.log_m,
-                       w=self.wv.data_ptr(), v=self.wv.data_ptr() + C * cs, bbar=bbar_ptr, lw=plan.lw,
-                       rlk=self.ctx.rlk.data_ptr(), rot_left=self._k_left, rot_right=self._k_right,
+        return NagArgs(z=self.zstage.data_ptr(), rows=self.rows, cols=C, log_g=self.log_g, log_m=self.log_m,
+                       w=self.wv.data_ptr(), v=self.wv.data_ptr() + C * cs, bbar=self.bstage.data_ptr(),
+                       lw=plan.lw, rlk=self.ctx.rlk.data_ptr(), rot_left=self._k_left, rot_right=self._k_right,
                        rot_rows=self._k_rows, mask_pt=self._mask(plan.lw, plan.mask_scale).data_ptr(),
                        consts=self.consts_dev.data_ptr(), grad=self.grad.data_ptr(), phase=phase)
 
@@ -300,61 +324,63 @@ class FusedTrainer:
         self.consts_host.copy_(torch.from_numpy(plan.consts.view(np.int64)))
         self.consts_dev.copy_(self.consts_host, non_blocking=True)
 
-    def _z_ptr(self, b: int) -> int:
-        if self.z_on_host:
-            self.zstage.copy_(self.z[b], non_blocking=True)
-            return self.zstage.data_ptr()
-        return self.z[b].data_ptr()
+    def _stage(self, batch: int, bbar_index: int, with_bbar: bool = True):
+        src_z = self.z_host if self.host_stream else self.z
+        src_b = self.b_host if self.host_stream else self.bbar
+        self.zstage.copy_(src_z[batch], non_blocking=True)
+        if with_bbar:
+            self.bstage.copy_(src_b[bbar_index], non_blocking=True)
 
     def _run(self, args: NagArgs):
         stream = torch.cuda.current_stream().cuda_stream
-        if not self.use_graph:
+        if not self.use_graph or not self._warm:
+            # eager; the first eager run also allocates the driver workspace
             _lib.check(self.lib.helr_nag_iteration(self.ctx.handle, ctypes.byref(args), stream), "helr_nag_iteration")
+            self._warm = True
             return
-        key = (args.z, args.w, args.bbar, args.lw, args.phase, args.mask_pt)
-        if self._graph is None or self._graph_key != key:
-            if self._graph is not None:
-                self.lib.helr_nag_graph_destroy(self._graph)
-                self._graph = None
-            # one eager run first allocates the driver workspace outside capture
-            if not getattr(self, "_warm", False):
-                _lib.check(self.lib.helr_nag_iteration(self.ctx.handle, ctypes.byref(args), stream),
-                           "helr_nag_iteration")
-                self._warm = True
-                return
+        key = (args.lw, args.phase, args.mask_pt)
+        g = self._graphs.get(key)
+        if g is None:
             g = ctypes.c_void_p()
             _lib.check(self.lib.helr_nag_graph_capture(self.ctx.handle, ctypes.byref(args), stream, ctypes.byref(g)),
                        "helr_nag_graph_capture")
-            self._graph, self._graph_key = g, key
-        _lib.check(self.lib.helr_nag_graph_launch(self._graph, stream), "helr_nag_graph_launch")
+            self._graphs[key] = g
+        _lib.check(self.lib.helr_nag_graph_launch(g, stream), "helr_nag_graph_launch")
 
     def iterate(self, batch: Optional[int] = None) -> dict:
-        """One NAG iteration (mini-batch: batch ``t mod n_batches``; full: all)."""
+        """One NAG iteration (mini-batch: batch ``t mod n_batches``; full: all),
+        issued on the trainer's stream."""
+        with torch.cuda.stream(self.stream):
+            return self._iterate(batch)
+
+    def _iterate(self, batch: Optional[int]) -> dict:
         refreshed = self._refresh_if_needed()
         if self.mode == "mini_batch":
             b = (self.t % self.n_batches) if batch is None else batch
-            lo = b * self.batch_rows
-            gamma_rows = min(self.batch_rows, self.ds.n_samples - lo)
+            gamma_rows = min(self.batch_rows, self.ds.n_samples - b * self.batch_rows)
         else:
+            b = 0
             gamma_rows = self.ds.n_samples
         lr, eta, gamma, mult = self.step_scalars(self.t, gamma_rows)
         plan = plan_iteration(self.ck, self.level, self.s_w, self.s_v, self.s_z, self.s_b, self.qpoly, mult, eta)
         self._upload_consts(plan)
-        cs = self.bbar[0, 0].numel() * 8
         if self.mode == "mini_batch":
-            args = self._args(self._z_ptr(b), self.bbar[b].data_ptr(), plan, 0)
-            self._run(args)
+            self._stage(b, b)
+            self._run(self._args(plan, 0))
         else:
             for bb in range(self.n_batches):
-                args = self._args(self._z_ptr(bb), self.bbar[0].data_ptr(), plan, 1 if bb == 0 else 2)
-                self._run(args)
-            args = self._args(self._z_ptr(0), self.bbar[0].data_ptr(), plan, 3)
-            self._run(args)
+                self._stage(bb, 0, with_bbar=(bb == 0))
+                self._run(self._args(plan, 1 if bb == 0 else 2))
+            self._run(self._args(plan, 3))
         level_start = self.level
         self.level -= ITER_DEPTH
         self.s_w = self.s_v = plan.s_out
         self.alpha0, self.alpha1 = self.alpha1, next_alpha(self.alpha1)
         self.t += 1
+        if self.host_stream:
+            # the step's result leaves the device: the updated weight ciphertexts
+            lv = self.level + 1
+            self.w_host[:, :, :lv].copy_(self.wv[:, :, :lv], non_blocking=True)
         return dict(iteration=self.t, lr=lr, eta=eta, gamma=gamma, level_start=level_start,
                     level_after=self.level, refreshed=refreshed)
 
@@ -364,10 +390,11 @@ class FusedTrainer:
         enctrain.py:266-289, without the exact replication check)."""
         ctx, lay = self.ctx, self.layout
         C = self.cols
-        out = torch.empty((C, self.ck.n), dtype=torch.int64, device=ctx.device)
-        ctx._call("helr_decrypt", ctx.sk.data_ptr(), self.wv.data_ptr(), C, self.level, out.data_ptr(),
-                  torch.cuda.current_stream().cuda_stream)
-        coef = out.cpu().numpy()
+        with torch.cuda.stream(self.stream):
+            out = torch.empty((C, self.ck.n), dtype=torch.int64, device=ctx.device)
+            ctx._call("helr_decrypt", ctx.sk.data_ptr(), self.wv.data_ptr(), C, self.level, out.data_ptr(),
+                      self.stream.cuda_stream)
+            coef = out.cpu().numpy()
         segs = []
         for j in range(C):
             grid = ctx.encoder.decode(coef[j], self.s_w).reshape(lay.m, lay.g)
@@ -375,6 +402,6 @@ class FusedTrainer:
         return np.concatenate(segs)[: lay.cols]
 
     def close(self):
-        if self._graph is not None:
-            self.lib.helr_nag_graph_destroy(self._graph)
-            self._graph = None
+        for g in self._graphs.values():
+            self.lib.helr_nag_graph_destroy(g)
+        self._graphs.clear()

@@ -1,0 +1,63 @@
+"""End-to-end value parity: the fused GPU trainer (real RNS-CKKS, refresh
+stand-in every iteration) against golden weight traces produced by the
+REFERENCE simulator (tests/golden, tools/make_goldens.py).  BASELINE bar:
+decrypted weights and AUC within 1e-6 absolute."""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_2406_13221_b200 import data
+from paper_2406_13221_b200.ckks import GpuContext
+from paper_2406_13221_b200.driver import FusedTrainer
+from paper_2406_13221_b200.optimizer import auroc
+from paper_2406_13221_b200.params import CkksParams
+from pathlib import Path
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+TOL = 1e-6
+
+
+def _run(name, ds, log_n, rows, blocks, mode, n_iters, use_graph=False):
+    gold = np.load(GOLD / f"{name}.npz")
+    ck = CkksParams.generate(log_n=log_n, n_q=8, dnum=3)
+    ctx = GpuContext(ck, seed=2, max_batch=8)
+    tr = FusedTrainer(ctx, ds, rows_per_block=rows, blocks_per_batch=blocks, mode=mode, use_graph=use_graph)
+    its = list(gold["iterations"])
+    worst_w, worst_auc = 0.0, 0.0
+    for t in range(1, n_iters + 1):
+        tr.iterate()
+        if t in its:
+            k = its.index(t)
+            w = tr.weights()
+            worst_w = max(worst_w, float(np.max(np.abs(w - gold["weights"][k]))))
+            worst_auc = max(worst_auc, abs(auroc(ds.y, ds.X @ w) - float(gold["auc"][k])))
+    tr.close()
+    return worst_w, worst_auc
+
+
+def test_toy_all_iterations():
+    w, a = _run("toy", data.toy_dataset(), 13, 128, 1, "mini_batch", 24)
+    print(f"toy: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
+    assert w < TOL and a < TOL
+
+
+def test_toy_with_cuda_graph():
+    w, a = _run("toy", data.toy_dataset(), 13, 128, 1, "mini_batch", 24, use_graph=True)
+    assert w < TOL and a < TOL
+
+
+def test_medium_first_iterations():
+    w, a = _run("medium", data.medium_dataset(), 15, 1024, 1, "mini_batch", 32)
+    print(f"medium: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
+    assert w < TOL and a < TOL
+
+
+def test_paper_mini_first_iterations():
+    w, a = _run("paper_mini", data.paper_dataset(), 16, 128, 8, "mini_batch", 16, use_graph=True)
+    print(f"paper_mini: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
+    assert w < TOL and a < TOL
