@@ -259,24 +259,27 @@ def main():
         ms = float(t.item())
     value = steps * ws / (ms / 1000.0)
 
-    # ---------------- live per-kernel attribution (eager launches, CUDA events)
-    tr_graph = tr.use_graph
-    tr.use_graph = False
+    # ---------------- live per-kernel attribution: CUDA events recorded inside a
+    # captured graph (no host launch gaps), one category pair per launch
     c0 = lib.helr_launch_count()
-    lib.helr_prof_enable(1)
-    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    pe0.record(stream)
-    for _ in range(args.profile_steps):
-        tr.iterate()
-    pe1.record(stream)
-    lib.helr_prof_enable(0)
     msa = (ctypes.c_double * 8)()
     bya = (ctypes.c_double * 8)()
     cna = (ctypes.c_int * 8)()
-    lib.helr_prof_collect(msa, bya, cna)
+    tot_ms, tot_by, tot_cn = [0.0] * 8, [0.0] * 8, [0] * 8
+    prof_ms = 0.0
+    for _ in range(args.profile_steps):
+        pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pe0.record(stream)
+        tr.profile_iteration()
+        pe1.record(stream)
+        lib.helr_prof_collect(msa, bya, cna)
+        prof_ms += pe0.elapsed_time(pe1)
+        for i in range(8):
+            tot_ms[i] += msa[i]
+            tot_by[i] += bya[i]
+            tot_cn[i] += cna[i]
     launches_per_step = (lib.helr_launch_count() - c0) / args.profile_steps
-    prof_ms = pe0.elapsed_time(pe1)
-    tr.use_graph = tr_graph
+    msa, bya, cna = tot_ms, tot_by, tot_cn
     cats = {CATS[i]: {"ms": msa[i] / args.profile_steps, "launches": cna[i] / args.profile_steps,
                       "gb": bya[i] / args.profile_steps / 1e9} for i in range(8)}
     dom = max(range(8), key=lambda i: msa[i])
@@ -285,7 +288,7 @@ def main():
     traffic = ncu_traffic().get(CATS[dom])
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": CATS[dom], "peak_kind": peak_kind,
-                "share_of_step": msa[dom] / prof_ms,
+                "share_of_step": (msa[dom] / args.profile_steps) / (ms / steps),
                 "algorithmic_bytes_per_launch": bya[dom] / cna[dom],
                 "avg_launch_ms": msa[dom] / cna[dom]}
     step_gb = sum(bya) / args.profile_steps / 1e9

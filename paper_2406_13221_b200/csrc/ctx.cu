@@ -12,6 +12,13 @@ typedef unsigned __int128 h128;
 static thread_local std::string g_err;
 
 void set_error(const std::string& msg) { g_err = msg; }
+// Clear an error left by an earlier, unrelated runtime call on this thread so
+// it is not blamed on the next launch; report it once on stderr.
+void clear_stale_error(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[helr] stale CUDA error before %s: %s\n", where, cudaGetErrorString(e));
+}
+
 bool cuda_ok(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return true;
     g_err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -119,10 +126,11 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
 
     // ---- build every table on the host, one contiguous upload -----------
     std::vector<u64> h;
-    auto put = [&](size_t words) { size_t o = h.size(); h.resize(o + words); return o; };
+    auto put = [&](size_t words) { size_t o = (h.size() + 1) & ~(size_t)1; h.resize(o + words); return o; };  // 16-byte aligned
     size_t o_q = put(LK), o_b1 = put(LK), o_b0 = put(LK);
-    size_t o_tw = put((size_t)LK * n), o_tws = put((size_t)LK * n);
-    size_t o_itw = put((size_t)LK * n), o_itws = put((size_t)LK * n);
+    // twiddles as interleaved (w, floor(w 2^64 / q)) pairs: one 16-byte load per butterfly group
+    size_t o_tw = put(2 * (size_t)LK * n);
+    size_t o_itw = put(2 * (size_t)LK * n);
     size_t o_ni = put(LK), o_nis = put(LK), o_i1 = put(LK), o_i1s = put(LK);
     for (int p = 0; p < LK; p++) {
         u64 q = primes[p];
@@ -137,15 +145,15 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
         for (int k = 0; k < n; k++) {
             unsigned e = hbrv((unsigned)k, log_n);
             u64 w = pw[e], iw = ipw[e];
-            h[o_tw + (size_t)p * n + k] = w;
-            h[o_tws + (size_t)p * n + k] = hshoup(w, q);
-            h[o_itw + (size_t)p * n + k] = iw;
-            h[o_itws + (size_t)p * n + k] = hshoup(iw, q);
+            h[o_tw + 2 * ((size_t)p * n + k)] = w;
+            h[o_tw + 2 * ((size_t)p * n + k) + 1] = hshoup(w, q);
+            h[o_itw + 2 * ((size_t)p * n + k)] = iw;
+            h[o_itw + 2 * ((size_t)p * n + k) + 1] = hshoup(iw, q);
         }
         u64 ni = hinv((u64)n, q);
         h[o_ni + p] = ni;
         h[o_nis + p] = hshoup(ni, q);
-        u64 i1 = hmul(h[o_itw + (size_t)p * n + 1], ni, q);
+        u64 i1 = hmul(h[o_itw + 2 * ((size_t)p * n + 1)], ni, q);
         h[o_i1 + p] = i1;
         h[o_i1s + p] = hshoup(i1, q);
     }
@@ -212,7 +220,7 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
         cudaFree(c->d_tab); delete c; return HELR_ECUDA;
     }
     const u64* d = c->d_tab;
-    c->t = Tables{d + o_q, d + o_b1, d + o_b0, d + o_tw, d + o_tws, d + o_itw, d + o_itws,
+    c->t = Tables{d + o_q, d + o_b1, d + o_b0, d + o_tw, d + o_itw,
                   d + o_ni, d + o_nis, d + o_i1, d + o_i1s, log_n, n, L, K, alpha, c->beta};
     c->qlinv = d + o_ql; c->qlinv_sh = d + o_qls;
     c->md_phinv = d + o_phi; c->md_phinv_sh = d + o_phis;

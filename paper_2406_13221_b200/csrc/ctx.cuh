@@ -8,16 +8,15 @@
 #include "modarith.cuh"
 
 #define HELR_MAXP 64
+#define HELR_MAXLIMBS 128  // entries of one LimbMap (one batched NTT launch)
 
 // Per-prime scalar tables, passed by value to kernels (all device pointers).
 struct Tables {
     const u64* q;        // [LK]
     const u64* br1;      // floor(2^128/q) high word
     const u64* br0;      // low word
-    const u64* tw;       // [LK][N]  psi^brv(k)
-    const u64* tw_sh;
-    const u64* itw;      // [LK][N]  psi^-brv(k)
-    const u64* itw_sh;
+    const u64* tw;       // [LK][N][2]  (psi^brv(k), Shoup quotient)
+    const u64* itw;      // [LK][N][2]  (psi^-brv(k), Shoup quotient)
     const u64* ninv;     // [LK]  N^-1
     const u64* ninv_sh;
     const u64* itw1n;    // [LK]  psi^-brv(1) * N^-1  (last inverse stage)
@@ -29,8 +28,8 @@ struct Tables {
 // base + z*item_stride + off[i]*N and uses prime prime[i].
 struct LimbMap {
     int count;
-    unsigned char off[HELR_MAXP];
-    unsigned char prime[HELR_MAXP];
+    unsigned char off[HELR_MAXLIMBS];
+    unsigned char prime[HELR_MAXLIMBS];
 };
 
 struct helr_ctx {
@@ -65,6 +64,7 @@ struct helr_ctx {
 
 void set_error(const std::string& msg);
 bool cuda_ok(cudaError_t e, const char* what);
+void clear_stale_error(const char* where);
 
 // helpers shared by the .cu files
 inline LimbMap limb_range(int first_prime, int count, int first_off = 0) {

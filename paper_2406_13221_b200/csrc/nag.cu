@@ -171,11 +171,13 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
 }
 
 extern "C" int helr_nag_iteration(helr_ctx* c, const helr_nag_args* a, void* stream) {
+    clear_stale_error("helr_nag_iteration");
     if (!c || !a) { set_error("null argument"); return HELR_EINVAL; }
     return nag_run(c, a, (cudaStream_t)stream);
 }
 
 extern "C" int helr_nag_graph_capture(helr_ctx* c, const helr_nag_args* a, void* stream, void** graph_exec) {
+    clear_stale_error("helr_nag_graph_capture");
     if (!c || !a || !graph_exec) { set_error("null argument"); return HELR_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
     u64* ws = nullptr;
@@ -195,12 +197,14 @@ extern "C" int helr_nag_graph_capture(helr_ctx* c, const helr_nag_args* a, void*
 }
 
 extern "C" int helr_nag_graph_launch(void* graph_exec, void* stream) {
+    clear_stale_error("helr_nag_graph_launch");
     if (!graph_exec) { set_error("null graph"); return HELR_EINVAL; }
     if (!cuda_ok(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream), "graph launch")) return HELR_ECUDA;
     return HELR_OK;
 }
 
 extern "C" int helr_nag_graph_destroy(void* graph_exec) {
+    clear_stale_error("helr_nag_graph_destroy");
     if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
     return HELR_OK;
 }

@@ -43,8 +43,88 @@ __device__ __forceinline__ int spread_index(int s, int lo, int log_r) {
 }
 
 // Loader: u64 operator()(int z, int li, int prime, int off) const
+//         (+ optional kVec / load2 for 16-byte contiguous pairs)
 // Storer: void operator()(int z, int li, int prime, int off, u64 v) const
+//         (+ optional kVec / store2)
 // grid: x = sub-transform tiles, y = limb index in map, z = batch item.
+template <class F, class = void>
+struct has_vec { static constexpr bool value = false; };
+template <class F>
+struct has_vec<F, decltype((void)F::kVec)> { static constexpr bool value = F::kVec; };
+
+// One radix-2 stage on a thread's R registers: pairs (i, i + 2^H), the
+// twiddle shared by every pair with the same i >> (H + 1).  H is a template
+// parameter so every register index is static (no local-memory arrays).
+template <int R, int H>
+__device__ __forceinline__ void fwd_stage(u64 (&x)[R], const ulonglong2* __restrict__ W2, int tb0, u64 q, u64 q2) {
+#pragma unroll
+    for (int j = 0; j < (R >> (H + 1)); j++) {
+        const ulonglong2 w = __ldg(W2 + tb0 + j);
+#pragma unroll
+        for (int t = 0; t < (1 << H); t++) {
+            const int i = (j << (H + 1)) + t;
+            u64 u = x[i];
+            u = u >= q2 ? u - q2 : u;
+            const u64 v = shoup_lazy(x[i + (1 << H)], w.x, w.y, q);
+            x[i] = u + v;
+            x[i + (1 << H)] = u + q2 - v;
+        }
+    }
+}
+template <int R, int H>
+__device__ __forceinline__ void inv_stage(u64 (&x)[R], const ulonglong2* __restrict__ W2, int tb0, u64 q, u64 q2) {
+#pragma unroll
+    for (int j = 0; j < (R >> (H + 1)); j++) {
+        const ulonglong2 w = __ldg(W2 + tb0 + j);
+#pragma unroll
+        for (int t = 0; t < (1 << H); t++) {
+            const int i = (j << (H + 1)) + t;
+            const u64 u = x[i], v = x[i + (1 << H)];
+            const u64 sum = u + v;
+            x[i] = sum >= q2 ? sum - q2 : sum;
+            x[i + (1 << H)] = shoup_lazy(u + q2 - v, w.x, w.y, q);
+        }
+    }
+}
+// last inverse stage (psi^-brv(1)) with N^-1 folded into both outputs
+template <int R, int H>
+__device__ __forceinline__ void inv_last_stage(u64 (&x)[R], u64 ni, u64 nis, u64 wl, u64 wls, u64 q, u64 q2) {
+#pragma unroll
+    for (int i = 0; i < R; i++) {
+        if (i & (1 << H)) continue;
+        const u64 u = x[i], v = x[i + (1 << H)];
+        x[i] = shoup_lazy(u + v, ni, nis, q);
+        x[i + (1 << H)] = shoup_lazy(u + q2 - v, wl, wls, q);
+    }
+}
+template <int R>
+__device__ __forceinline__ void fwd_stage_h(int h, u64 (&x)[R], const ulonglong2* W2, int tb0, u64 q, u64 q2) {
+    switch (h) {
+        case 0: fwd_stage<R, 0>(x, W2, tb0, q, q2); break;
+        case 1: if constexpr (R > 2) fwd_stage<R, 1>(x, W2, tb0, q, q2); break;
+        case 2: if constexpr (R > 4) fwd_stage<R, 2>(x, W2, tb0, q, q2); break;
+        default: if constexpr (R > 8) fwd_stage<R, 3>(x, W2, tb0, q, q2); break;
+    }
+}
+template <int R>
+__device__ __forceinline__ void inv_stage_h(int h, u64 (&x)[R], const ulonglong2* W2, int tb0, u64 q, u64 q2) {
+    switch (h) {
+        case 0: inv_stage<R, 0>(x, W2, tb0, q, q2); break;
+        case 1: if constexpr (R > 2) inv_stage<R, 1>(x, W2, tb0, q, q2); break;
+        case 2: if constexpr (R > 4) inv_stage<R, 2>(x, W2, tb0, q, q2); break;
+        default: if constexpr (R > 8) inv_stage<R, 3>(x, W2, tb0, q, q2); break;
+    }
+}
+template <int R>
+__device__ __forceinline__ void inv_last_h(int h, u64 (&x)[R], u64 ni, u64 nis, u64 wl, u64 wls, u64 q, u64 q2) {
+    switch (h) {
+        case 0: inv_last_stage<R, 0>(x, ni, nis, wl, wls, q, q2); break;
+        case 1: if constexpr (R > 2) inv_last_stage<R, 1>(x, ni, nis, wl, wls, q, q2); break;
+        case 2: if constexpr (R > 4) inv_last_stage<R, 2>(x, ni, nis, wl, wls, q, q2); break;
+        default: if constexpr (R > 8) inv_last_stage<R, 3>(x, ni, nis, wl, wls, q, q2); break;
+    }
+}
+
 template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, class Ld, class St>
 __global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R))
 ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
@@ -61,8 +141,7 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     const u64 q2 = 2 * q;
     const int n = 1 << a.log_n;
     const int s2 = a.log_n - LOG_T;  // used by column passes
-    const u64* W = (INV ? tb.itw : tb.tw) + (size_t)prime * n;
-    const u64* Wsh = (INV ? tb.itw_sh : tb.tw_sh) + (size_t)prime * n;
+    const ulonglong2* W2 = reinterpret_cast<const ulonglong2*>(INV ? tb.itw : tb.tw) + (size_t)prime * n;
 
     const int tid = threadIdx.x;
     int cc, s;
@@ -70,6 +149,7 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     else { s = tid % TPS; cc = tid / TPS; }
     const int sub = blockIdx.x * COLS + cc;  // global column / block index
     const int sub_id = IS_COL ? 0 : sub;
+    const int wrow = (1 << a.st0) + sub_id;  // twiddle index = (wrow << ls) + (k >> (qb + 1))
 
     auto goff = [&](int k) -> int {
         return IS_COL ? (sub + (k << s2)) : ((sub << LOG_T) + k);
@@ -81,17 +161,27 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     u64 x[R];
 #pragma unroll
     for (int g = 0; g < NG; g++) {
-        int lo;
-        if (!INV) {
-            const int hi = LOG_T - g * LOG_R;
-            lo = hi - LOG_R > 0 ? hi - LOG_R : 0;
-        } else {
-            lo = g * LOG_R < LOG_T - LOG_R ? g * LOG_R : LOG_T - LOG_R;
-        }
+        // free index bits of this register group: [lo, lo + LOG_R)
+        const int lo = !INV ? ((LOG_T - g * LOG_R - LOG_R) > 0 ? (LOG_T - g * LOG_R - LOG_R) : 0)
+                            : ((g * LOG_R < LOG_T - LOG_R) ? g * LOG_R : LOG_T - LOG_R);
         const int base = spread_index(s, lo, LOG_R);
         if (g == 0) {
+            if constexpr (!IS_COL && has_vec<Ld>::value) {
+                if (lo == 0) {
 #pragma unroll
-            for (int i = 0; i < R; i++) x[i] = ld(z, li, prime, goff(base + (i << lo)));
+                    for (int i = 0; i < R; i += 2) {
+                        const ulonglong2 v = ld.load2(z, li, prime, goff(base + i));
+                        x[i] = v.x;
+                        x[i + 1] = v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < R; i++) x[i] = ld(z, li, prime, goff(base + (i << lo)));
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < R; i++) x[i] = ld(z, li, prime, goff(base + (i << lo)));
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < R; i++) x[i] = sm[sidx(base + (i << lo))];
@@ -103,57 +193,42 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
 #pragma unroll
             for (int qb = qhi; qb >= qlo; qb--) {
                 const int ls = LOG_T - 1 - qb;
-                const int half = 1 << (qb - lo);
-#pragma unroll
-                for (int i = 0; i < R; i++) {
-                    if (i & half) continue;
-                    const int k = base + (i << lo);
-                    const int widx = (((1 << a.st0) + sub_id) << ls) + (k >> (qb + 1));
-                    const u64 w = __ldg(W + widx), wsh = __ldg(Wsh + widx);
-                    u64 u = x[i];
-                    u = u >= q2 ? u - q2 : u;
-                    const u64 t = shoup_lazy(x[i + half], w, wsh, q);
-                    x[i] = u + t;
-                    x[i + half] = u + q2 - t;
-                }
+                fwd_stage_h<R>(qb - lo, x, W2, (wrow << ls) + (base >> (qb + 1)), q, q2);
             }
         } else {
             const int qlo = g * LOG_R;
             const int qhi = (g + 1) * LOG_R < LOG_T ? (g + 1) * LOG_R - 1 : LOG_T - 1;
-            const bool last_stage_pass = (a.st0 == 0);
 #pragma unroll
             for (int qb = qlo; qb <= qhi; qb++) {
                 const int ls = LOG_T - 1 - qb;
-                const int half = 1 << (qb - lo);
-                const bool fold_ninv = last_stage_pass && ls == 0;
-#pragma unroll
-                for (int i = 0; i < R; i++) {
-                    if (i & half) continue;
-                    const int k = base + (i << lo);
-                    const u64 u = x[i], v = x[i + half];
-                    const u64 t = u + q2 - v;  // (0, 4q)
-                    if (fold_ninv) {
-                        x[i] = shoup_lazy(u + v, tb.ninv[prime], tb.ninv_sh[prime], q);
-                        x[i + half] = shoup_lazy(t, tb.itw1n[prime], tb.itw1n_sh[prime], q);
-                    } else {
-                        const int widx = (((1 << a.st0) + sub_id) << ls) + (k >> (qb + 1));
-                        const u64 w = __ldg(W + widx), wsh = __ldg(Wsh + widx);
-                        u64 sum = u + v;
-                        x[i] = sum >= q2 ? sum - q2 : sum;
-                        x[i + half] = shoup_lazy(t, w, wsh, q);
-                    }
+                if (a.st0 == 0 && ls == 0) {
+                    inv_last_h<R>(qb - lo, x, tb.ninv[prime], tb.ninv_sh[prime], tb.itw1n[prime], tb.itw1n_sh[prime],
+                                  q, q2);
+                } else {
+                    inv_stage_h<R>(qb - lo, x, W2, (wrow << ls) + (base >> (qb + 1)), q, q2);
                 }
             }
         }
         if (g == NG - 1) {
 #pragma unroll
             for (int i = 0; i < R; i++) {
-                u64 v = x[i];
                 if (a.final_out) {
+                    u64 v = x[i];
                     if (!INV) v = v >= q2 ? v - q2 : v;
-                    v = v >= q ? v - q : v;
+                    x[i] = v >= q ? v - q : v;
                 }
-                st(z, li, prime, goff(base + (i << lo)), v);
+            }
+            if constexpr (!IS_COL && has_vec<St>::value) {
+                if (lo == 0) {
+#pragma unroll
+                    for (int i = 0; i < R; i += 2) st.store2(z, li, prime, goff(base + i), make_ulonglong2(x[i], x[i + 1]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < R; i++) st(z, li, prime, goff(base + (i << lo)), x[i]);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < R; i++) st(z, li, prime, goff(base + (i << lo)), x[i]);
             }
         } else {
 #pragma unroll
@@ -165,6 +240,7 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
 
 // ---- plain functors: strided limb buffers -------------------------------
 struct LdBuf {
+    static constexpr bool kVec = true;
     const u64* base;
     long long item_stride;
     LimbMap map;  // copy of the offsets (small)
@@ -172,14 +248,21 @@ struct LdBuf {
     __device__ __forceinline__ u64 operator()(int z, int li, int, int off) const {
         return base[(size_t)z * item_stride + (size_t)map.off[li] * n + off];
     }
+    __device__ __forceinline__ ulonglong2 load2(int z, int li, int, int off) const {
+        return *reinterpret_cast<const ulonglong2*>(base + (size_t)z * item_stride + (size_t)map.off[li] * n + off);
+    }
 };
 struct StBuf {
+    static constexpr bool kVec = true;
     u64* base;
     long long item_stride;
     LimbMap map;
     int n;
     __device__ __forceinline__ void operator()(int z, int li, int, int off, u64 v) const {
         base[(size_t)z * item_stride + (size_t)map.off[li] * n + off] = v;
+    }
+    __device__ __forceinline__ void store2(int z, int li, int, int off, ulonglong2 v) const {
+        *reinterpret_cast<ulonglong2*>(base + (size_t)z * item_stride + (size_t)map.off[li] * n + off) = v;
     }
 };
 

@@ -102,24 +102,31 @@ static int launch_ew(helr_ctx* c, int op, const u64* a, const u64* b, u64* out, 
 }
 
 extern "C" int helr_add(helr_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_add");
     return launch_ew(c, EW_ADD, (const u64*)a, (const u64*)b, (u64*)out, count, level, s);
 }
 extern "C" int helr_sub(helr_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_sub");
     return launch_ew(c, EW_SUB, (const u64*)a, (const u64*)b, (u64*)out, count, level, s);
 }
 extern "C" int helr_add_const(helr_ctx* c, const uint64_t* a, const uint64_t* k, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_add_const");
     return launch_ew(c, EW_ADDC, (const u64*)a, (const u64*)k, (u64*)out, count, level, s);
 }
 extern "C" int helr_add_plain(helr_ctx* c, const uint64_t* a, const uint64_t* pt, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_add_plain");
     return launch_ew(c, EW_ADDPT, (const u64*)a, (const u64*)pt, (u64*)out, count, level, s);
 }
 extern "C" int helr_mul_const(helr_ctx* c, const uint64_t* a, const uint64_t* k, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_mul_const");
     return launch_ew(c, EW_MULC, (const u64*)a, (const u64*)k, (u64*)out, count, level, s);
 }
 extern "C" int helr_mul_plain(helr_ctx* c, const uint64_t* a, const uint64_t* pt, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_mul_plain");
     return launch_ew(c, EW_MULPT, (const u64*)a, (const u64*)pt, (u64*)out, count, level, s);
 }
 extern "C" int helr_imul(helr_ctx* c, const uint64_t* a, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_imul");
     return launch_ew(c, EW_IMUL, (const u64*)a, nullptr, (u64*)out, count, level, s);
 }
 
@@ -127,6 +134,7 @@ extern "C" int helr_imul(helr_ctx* c, const uint64_t* a, uint64_t* out, int coun
 // NTT entry points
 extern "C" int helr_ntt_fwd(helr_ctx* c, uint64_t* data, int first_prime, int n_limbs, int count, int64_t stride,
                             void* s) {
+    clear_stale_error("helr_ntt_fwd");
     if (first_prime < 0 || n_limbs < 1 || first_prime + n_limbs > c->LK) { set_error("bad limb range"); return HELR_EINVAL; }
     if (count < 1) return HELR_OK;
     LimbMap m = limb_range(first_prime, n_limbs);
@@ -136,6 +144,7 @@ extern "C" int helr_ntt_fwd(helr_ctx* c, uint64_t* data, int first_prime, int n_
 }
 extern "C" int helr_ntt_inv(helr_ctx* c, uint64_t* data, int first_prime, int n_limbs, int count, int64_t stride,
                             void* s) {
+    clear_stale_error("helr_ntt_inv");
     if (first_prime < 0 || n_limbs < 1 || first_prime + n_limbs > c->LK) { set_error("bad limb range"); return HELR_EINVAL; }
     if (count < 1) return HELR_OK;
     LimbMap m = limb_range(first_prime, n_limbs);
@@ -155,6 +164,7 @@ __global__ void k_fill_secret(u64* sk, int n, int LK, u64 seed, Tables tb) {
 }
 
 extern "C" int helr_keygen_secret(helr_ctx* c, uint64_t* sk, uint64_t seed, void* s) {
+    clear_stale_error("helr_keygen_secret");
     k_fill_secret<<<blocks_for(c->n, 256), 256, 0, S(s)>>>((u64*)sk, c->n, c->LK, seed, c->t);
     CHECK_KERNEL("keygen_secret");
     LimbMap m = limb_range(0, c->LK);
@@ -200,6 +210,7 @@ __global__ void k_key_combine(u64* evk, const u64* sk, int n, int log_n, int L, 
 
 extern "C" int helr_keygen_switch(helr_ctx* c, const uint64_t* sk, int64_t galois, uint64_t* evk, uint64_t seed,
                                   uint64_t key_id, void* s) {
+    clear_stale_error("helr_keygen_switch");
     if (galois != 0 && ((galois & 1) == 0 || galois < 0)) { set_error("galois element must be odd and positive"); return HELR_EINVAL; }
     galois = galois % (2ll * c->n);
     dim3 g1(blocks_for(c->n, 256), c->beta);
@@ -259,6 +270,7 @@ static int encrypt_dev(helr_ctx* c, const u64* sk, const long long* msg, u64* ct
 
 extern "C" int helr_encrypt(helr_ctx* c, const uint64_t* sk, const int64_t* msg, uint64_t* ct, int count, int level,
                             uint64_t seed, uint64_t first_id, void* s) {
+    clear_stale_error("helr_encrypt");
     if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
     if (count < 1) return HELR_OK;
     return encrypt_dev(c, (const u64*)sk, (const long long*)msg, (u64*)ct, count, level, seed, first_id, S(s));
@@ -299,6 +311,7 @@ static int decrypt_dev(helr_ctx* c, const u64* sk, const u64* ct, int count, lon
 
 extern "C" int helr_decrypt(helr_ctx* c, const uint64_t* sk, const uint64_t* ct, int count, int level, int64_t* out,
                             void* s) {
+    clear_stale_error("helr_decrypt");
     if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
     for (int b0 = 0; b0 < count; b0 += c->max_batch) {
         int nb = count - b0 < c->max_batch ? count - b0 : c->max_batch;
@@ -317,6 +330,7 @@ __global__ void k_plain_fill(const long long* msg, u64* pt, int n, int L, int nl
     }
 }
 extern "C" int helr_encode_plain(helr_ctx* c, const int64_t* msg, uint64_t* pt, int count, int level, void* s) {
+    clear_stale_error("helr_encode_plain");
     if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
     if (count < 1) return HELR_OK;
     dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
@@ -331,6 +345,7 @@ extern "C" int helr_encode_plain(helr_ctx* c, const int64_t* msg, uint64_t* pt, 
 
 extern "C" int helr_refresh(helr_ctx* c, const uint64_t* sk, const uint64_t* a, int in_level, double ratio,
                             uint64_t* out, int out_level, int count, uint64_t seed, uint64_t first_id, void* s) {
+    clear_stale_error("helr_refresh");
     if (in_level < 0 || in_level >= c->L || out_level < 0 || out_level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
     // workspace: [B][N] u64 scratch + [B][N] int64 message
     const int chunk = c->max_batch;
@@ -429,6 +444,7 @@ int op_rescale(helr_ctx* c, const u64* a, long long as, u64* out, long long os, 
 }
 
 extern "C" int helr_rescale(helr_ctx* c, const uint64_t* a, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_rescale");
     const long long cs = 2ll * c->L * c->n;
     return op_rescale(c, (const u64*)a, cs, (u64*)out, cs, count, level, S(s));
 }
@@ -654,19 +670,23 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
         k_modup<<<g, 128, 0, s>>>(a, c->t);
         CHECK_KERNEL("ks modup");
     }
-    // 3) NTT of the converted limbs, per digit
-    for (int j = 0; j < nd; j++) {
-        const int lo = j * c->alpha, hi = lo + c->alpha < nl ? lo + c->alpha : nl;
+    // 3) NTT of every converted limb of every digit (one launch per 128 limbs)
+    {
         LimbMap m;
         m.count = 0;
-        for (int e = 0; e < ne; e++) {
-            if (e >= lo && e < hi) continue;
-            m.off[m.count] = (unsigned char)e;
-            m.prime[m.count] = (unsigned char)(e < nl ? e : L + (e - nl));
-            m.count++;
+        for (int j = 0; j < nd; j++) {
+            const int lo = j * c->alpha, hi = lo + c->alpha < nl ? lo + c->alpha : nl;
+            for (int e = 0; e < ne; e++) {
+                if (e >= lo && e < hi) continue;
+                m.off[m.count] = (unsigned char)(j * c->LK + e);
+                m.prime[m.count] = (unsigned char)(e < nl ? e : L + (e - nl));
+                if (++m.count == HELR_MAXLIMBS) {
+                    ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s);
+                    m.count = 0;
+                }
+            }
         }
-        u64* base = w.ext + (size_t)j * w.ext_ds;
-        ntt_buffers<false>(c, base, w.ext_s, base, w.ext_s, m, B, s);
+        if (m.count) ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s);
         CHECK_LAUNCH("ks modup ntt");
     }
     // 4) inner product with the key
@@ -679,14 +699,13 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
     // 5) ModDown: INTT of the P limbs (both polys), conversion, NTT, combine
     {
         LimbMap m;
-        m.count = K;
-        for (int k = 0; k < K; k++) { m.off[k] = (unsigned char)(nl + k); m.prime[k] = (unsigned char)(L + k); }
-        // items: (b, poly) with poly stride ne*N inside acc item
-        // run per poly to keep a single item stride
-        for (int poly = 0; poly < 2; poly++) {
-            u64* base = w.acc + (size_t)poly * ne * n;
-            ntt_buffers<true>(c, base, w.acc_s, base, w.acc_s, m, B, s);
-        }
+        m.count = 2 * K;  // P limbs of both polynomials in one launch
+        for (int poly = 0; poly < 2; poly++)
+            for (int k = 0; k < K; k++) {
+                m.off[poly * K + k] = (unsigned char)(poly * ne + nl + k);
+                m.prime[poly * K + k] = (unsigned char)(L + k);
+            }
+        ntt_buffers<true>(c, w.acc, w.acc_s, w.acc, w.acc_s, m, B, s);
         CHECK_LAUNCH("ks moddown intt");
         dim3 g(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, 2 * B);
         {
@@ -695,11 +714,14 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
                                              c->md_phmod, c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
             CHECK_KERNEL("ks moddown conv");
         }
-        LimbMap mq = limb_range(0, nl);
-        for (int poly = 0; poly < 2; poly++) {
-            u64* base = w.mdc + (size_t)poly * L * n;
-            ntt_buffers<false>(c, base, w.mdc_s, base, w.mdc_s, mq, B, s);
-        }
+        LimbMap mq;
+        mq.count = 2 * nl;
+        for (int poly = 0; poly < 2; poly++)
+            for (int i = 0; i < nl; i++) {
+                mq.off[poly * nl + i] = (unsigned char)(poly * L + i);
+                mq.prime[poly * nl + i] = (unsigned char)i;
+            }
+        ntt_buffers<false>(c, w.mdc, w.mdc_s, w.mdc, w.mdc_s, mq, B, s);
         CHECK_LAUNCH("ks moddown ntt");
         dim3 g2(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, nl, 2 * B);
         {
@@ -773,6 +795,7 @@ int op_mul_relin_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, 
 
 extern "C" int helr_mul_relin(helr_ctx* c, const uint64_t* a, const uint64_t* b, const uint64_t* rlk, uint64_t* out,
                               int count, int level, void* s) {
+    clear_stale_error("helr_mul_relin");
     const long long cs = 2ll * c->L * c->n;
     return op_mul_relin_sum(c, (const u64*)a, cs, 0, (const u64*)b, cs, 0, 1, (const u64*)rlk, (u64*)out, cs, count,
                             level, S(s));
@@ -799,6 +822,7 @@ int op_rotate(helr_ctx* c, const u64* a, long long as, long long galois, const u
 
 extern "C" int helr_rotate(helr_ctx* c, const uint64_t* a, int64_t galois, const uint64_t* gk, uint64_t* out, int count,
                            int level, int accumulate, void* s) {
+    clear_stale_error("helr_rotate");
     const long long cs = 2ll * c->L * c->n;
     return op_rotate(c, (const u64*)a, cs, (long long)galois, (const u64*)gk, (u64*)out, cs, count, level, accumulate,
                      S(s));

@@ -1,4 +1,5 @@
 // prof.cu — event-pair recorder behind prof.cuh and its C ABI.
+#include <cstdio>
 #include <vector>
 
 #include "../../include/helr_ckks.h"
@@ -36,14 +37,24 @@ extern "C" unsigned long long helr_launch_count(void) { return g_launches; }
 
 void prof_begin(int cat, double bytes, cudaStream_t s) {
     Rec r{cat, bytes, take(), take()};
-    cudaEventRecord(r.a, s);
+    cudaError_t e = cudaEventRecordWithFlags(r.a, s, cudaEventRecordExternal);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "[helr prof] cudaEventRecord(begin) failed: %s\n", cudaGetErrorString(e));
+        cudaGetLastError();
+        return;
+    }
     g_recs.push_back(r);
     g_open = (int)g_recs.size() - 1;
 }
 
 void prof_end(cudaStream_t s) {
     if (g_open < 0) return;
-    cudaEventRecord(g_recs[g_open].b, s);
+    cudaError_t e = cudaEventRecordWithFlags(g_recs[g_open].b, s, cudaEventRecordExternal);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "[helr prof] cudaEventRecord(end) failed: %s\n", cudaGetErrorString(e));
+        cudaGetLastError();
+        g_recs.pop_back();
+    }
     g_open = -1;
 }
 
@@ -59,7 +70,7 @@ extern "C" int helr_prof_collect(double* ms, double* bytes, int* launches) {
     for (int c = 0; c < PROF_NCAT; c++) { ms[c] = 0; bytes[c] = 0; launches[c] = 0; }
     for (auto& r : g_recs) {
         float t = 0.f;
-        cudaEventElapsedTime(&t, r.a, r.b);
+        if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) { cudaGetLastError(); t = 0.f; }
         ms[r.cat] += t;
         bytes[r.cat] += r.bytes;
         launches[r.cat] += 1;

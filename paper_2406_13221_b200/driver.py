@@ -347,6 +347,26 @@ class FusedTrainer:
             self._graphs[key] = g
         _lib.check(self.lib.helr_nag_graph_launch(g, stream), "helr_nag_graph_launch")
 
+    def profile_iteration(self, batch: Optional[int] = None) -> dict:
+        """One iteration replayed from a freshly captured graph whose kernels are
+        bracketed by the library's category events (helr_prof_*), so the
+        per-category device times carry no host launch gaps."""
+        lib = self.lib
+        lib.helr_prof_enable.argtypes = [ctypes.c_int]
+        saved, self._graphs = self._graphs, {}
+        use, self.use_graph = self.use_graph, True
+        warm, self._warm = self._warm, True
+        lib.helr_prof_enable(1)
+        try:
+            info = self.iterate(batch)
+        finally:
+            lib.helr_prof_enable(0)
+            for g in self._graphs.values():
+                torch.cuda.synchronize()
+                lib.helr_nag_graph_destroy(g)
+            self._graphs, self.use_graph, self._warm = saved, use, warm
+        return info
+
     def iterate(self, batch: Optional[int] = None) -> dict:
         """One NAG iteration (mini-batch: batch ``t mod n_batches``; full: all),
         issued on the trainer's stream."""
