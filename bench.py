@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--cpu-iters", type=int, default=200, help="bounded CPU-baseline sample (iterations)")
     p.add_argument("--cpu-rns", action="store_true", help="also time the CPU RNS-CKKS oracle (1 iteration)")
     p.add_argument("--profile-steps", type=int, default=4)
+    p.add_argument("--dnum", type=int, default=None, help="override the key-switching digit count")
     return p.parse_args()
 
 
@@ -222,7 +223,7 @@ def main():
     lib.helr_launch_count.restype = ctypes.c_ulonglong
 
     t_setup = time.perf_counter()
-    ck = CkksParams.generate(log_n=wl["log_n"], n_q=wl["L"], dnum=wl["dnum"])
+    ck = CkksParams.generate(log_n=wl["log_n"], n_q=wl["L"], dnum=args.dnum or wl["dnum"])
     ctx = GpuContext(ck, seed=1, max_batch=max(8, wl["blocks"]))
     ds = make_dataset(wl["data"])
     tr = FusedTrainer(ctx, ds, rows_per_block=wl["rows"], blocks_per_batch=wl["blocks"], mode=wl["mode"],

@@ -126,7 +126,7 @@ __device__ __forceinline__ void inv_last_h(int h, u64 (&x)[R], u64 ni, u64 nis, 
 }
 
 template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, class Ld, class St>
-__global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R))
+__global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R), ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 256 ? 4 : 1)
 ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     using S = NttShape<LOG_T, LOG_R>;
     constexpr int T = S::T, R = S::R, NG = S::NG;

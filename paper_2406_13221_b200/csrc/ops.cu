@@ -220,7 +220,7 @@ extern "C" int helr_keygen_switch(helr_ctx* c, const uint64_t* sk, int64_t galoi
     const long long st = 2ll * c->LK * c->n;
     ntt_buffers<false>(c, (const u64*)evk, st, (u64*)evk, st, m, c->beta, S(s));
     CHECK_LAUNCH("keygen ntt");
-    dim3 g2(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, c->LK, c->beta);
+    dim3 g2(blocks_for(c->n, 256), c->LK, c->beta);
     k_key_combine<<<g2, 256, 0, S(s)>>>((u64*)evk, (const u64*)sk, c->n, c->log_n, c->L, c->LK, c->alpha, seed, key_id,
                                         (long long)galois, c->t, c->pmod);
     CHECK_KERNEL("keygen combine");
@@ -255,14 +255,14 @@ __global__ void k_enc_combine(u64* ct, const u64* sk, int n, int L, u64 seed, u6
 
 static int encrypt_dev(helr_ctx* c, const u64* sk, const long long* msg, u64* ct, int count, int level, u64 seed,
                        u64 first_id, cudaStream_t s) {
-    dim3 g1(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
+    dim3 g1(blocks_for(c->n, 256), count);
     k_enc_fill<<<g1, 256, 0, s>>>(ct, msg, c->n, c->L, level + 1, seed, first_id, c->eta, c->t);
     CHECK_KERNEL("encrypt fill");
     LimbMap m = limb_range(0, level + 1);
     const long long st = 2ll * c->L * c->n;
     ntt_buffers<false>(c, ct, st, ct, st, m, count, s);
     CHECK_LAUNCH("encrypt ntt");
-    dim3 g2(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, count);
+    dim3 g2(blocks_for(c->n, 256), level + 1, count);
     k_enc_combine<<<g2, 256, 0, s>>>(ct, sk, c->n, c->L, seed, first_id, c->t);
     CHECK_KERNEL("encrypt combine");
     return HELR_OK;
@@ -297,7 +297,7 @@ __global__ void k_center(const u64* v, long long* out, long long total, double r
 
 static int decrypt_dev(helr_ctx* c, const u64* sk, const u64* ct, int count, long long* out, double ratio,
                        u64* tmp, cudaStream_t s) {
-    dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
+    dim3 g(blocks_for(c->n, 256), count);
     k_dec_combine<<<g, 256, 0, s>>>(ct, sk, tmp, c->n, c->L, c->t);
     CHECK_KERNEL("decrypt combine");
     LimbMap m = limb_range(0, 1);
@@ -333,7 +333,7 @@ extern "C" int helr_encode_plain(helr_ctx* c, const int64_t* msg, uint64_t* pt, 
     clear_stale_error("helr_encode_plain");
     if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
     if (count < 1) return HELR_OK;
-    dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, count);
+    dim3 g(blocks_for(c->n, 256), count);
     k_plain_fill<<<g, 256, 0, S(s)>>>((const long long*)msg, (u64*)pt, c->n, c->L, level + 1, c->t);
     CHECK_KERNEL("plain fill");
     LimbMap m = limb_range(0, level + 1);
@@ -412,7 +412,7 @@ static int rescale_dev(helr_ctx* c, const u64* a, long long as, u64* out, long l
         ntt_launch<true>(c, ld, st, r, n, m, items, s);
         CHECK_LAUNCH("rescale intt");
     }
-    dim3 g1(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, items);
+    dim3 g1(blocks_for(n, 256), items);
     {
         ProfScope ps(PROF_RESCALE, 8.0 * n * items * (1 + l), s);
         k_rescale_conv<<<g1, 256, 0, s>>>(r, t, n, l, c->t);
@@ -421,7 +421,7 @@ static int rescale_dev(helr_ctx* c, const u64* a, long long as, u64* out, long l
     LimbMap m = limb_range(0, l);
     ntt_buffers<false>(c, t, (long long)l * n, t, (long long)l * n, m, items, s);
     CHECK_LAUNCH("rescale ntt");
-    dim3 g2(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, l, items);
+    dim3 g2(blocks_for(n, 256), l, items);
     {
         ProfScope ps(PROF_RESCALE, 8.0 * n * items * l * 3, s);
         k_rescale_final<<<g2, 256, 0, s>>>(a, as, t, out, os, n, L, l, c->qlinv, c->qlinv_sh, c->t);
@@ -479,6 +479,12 @@ struct ModUpArgs {
     const size_t* offs;// device array of modup offsets for this level (per digit)
     int n, log_n, nl, K, L, alpha;
 };
+// Two consecutive coefficients per thread, 16-byte accesses; register
+// arrays bounded by the template parameter (alpha / K <= MA).
+__device__ __forceinline__ ulonglong2 ld2(const u64* p) { return *reinterpret_cast<const ulonglong2*>(p); }
+__device__ __forceinline__ void st2(u64* p, u64 x, u64 y) { *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(x, y); }
+
+template <int MA>
 __global__ void k_modup(ModUpArgs a, Tables tb) {
     const int j = blockIdx.y, b = blockIdx.z;
     const int lo = j * a.alpha, hi = lo + a.alpha < a.nl ? lo + a.alpha : a.nl;
@@ -493,78 +499,83 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
     u64* ext = a.ext + (size_t)b * a.ext_item_stride + (size_t)j * a.ext_digit_stride;
     const u64* coef = a.coef + (size_t)b * a.coef_stride;
     const u64* d = a.d + (size_t)b * a.d_stride;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
-        u64 y[HELR_MAXP];
-        const int src_i = a.galois ? galois_perm(i, (u64)a.galois, a.log_n) : i;
-#pragma unroll 4
-        for (int k = 0; k < ns; k++) {
+    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= a.n) return;
+    u64 y0[MA], y1[MA];
+#pragma unroll
+    for (int k = 0; k < MA; k++) {
+        if (k < ns) {
             const int p = lo + k;
-            y[k] = shoup(coef[(size_t)p * a.n + i], hv[k], hvs[k], tb.q[p]);
-            ext[(size_t)p * a.n + i] = d[(size_t)p * a.n + src_i];
+            const ulonglong2 c = ld2(coef + (size_t)p * a.n + i);
+            y0[k] = shoup(c.x, hv[k], hvs[k], tb.q[p]);
+            y1[k] = shoup(c.y, hv[k], hvs[k], tb.q[p]);
+            if (a.galois) {
+                const u64* dp = d + (size_t)p * a.n;
+                st2(ext + (size_t)p * a.n + i, dp[galois_perm(i, (u64)a.galois, a.log_n)],
+                    dp[galois_perm(i + 1, (u64)a.galois, a.log_n)]);
+            } else {
+                *reinterpret_cast<ulonglong2*>(ext + (size_t)p * a.n + i) = ld2(d + (size_t)p * a.n + i);
+            }
         }
-        int t = 0;
-        for (int e = 0; e < ne; e++) {
-            if (e >= lo && e < hi) continue;
-            const int p = e < a.nl ? e : a.L + (e - a.nl);
-            const u64 q = tb.q[p];
-            u64 acc = 0;
-            for (int k = 0; k < ns; k++)
-                acc = add_mod(acc, shoup(y[k], hm[(size_t)k * nt + t], hms[(size_t)k * nt + t], q), q);
-            ext[(size_t)e * a.n + i] = acc;
-            t++;
+    }
+    int t = 0;
+    for (int e = 0; e < ne; e++) {
+        if (e >= lo && e < hi) continue;
+        const int p = e < a.nl ? e : a.L + (e - a.nl);
+        const u64 q = tb.q[p];
+        u64 s0 = 0, s1 = 0;
+#pragma unroll
+        for (int k = 0; k < MA; k++) {
+            if (k < ns) {
+                const u64 w = hm[(size_t)k * nt + t], ws = hms[(size_t)k * nt + t];
+                s0 = add_mod(s0, shoup(y0[k], w, ws, q), q);
+                s1 = add_mod(s1, shoup(y1[k], w, ws, q), q);
+            }
         }
+        st2(ext + (size_t)e * a.n + i, s0, s1);
+        t++;
     }
 }
 
 // inner product: acc[b][poly][e] = sum_j ext[b][j][e] * evk[j][poly][prime(e)]
-template <int BT>
+// block (64, <= 8): threadIdx.y = ciphertext, so the 8 warps of a block read
+// the same key words (one DRAM read, L1 hits for the rest).
 __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long ext_digit_stride, const u64* evk,
                            u64* acc, long long acc_item_stride, int n, int nl, int K, int L, int LK, int nd, int B,
                            Tables tb) {
     const int e = blockIdx.y;
+    const int b = blockIdx.z * blockDim.y + threadIdx.y;
+    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (b >= B || i >= n) return;
     const int p = e < nl ? e : L + (e - nl);
     const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        for (int b0 = 0; b0 < B; b0 += BT) {
-            u128v a0[BT], a1[BT];
-#pragma unroll
-            for (int x = 0; x < BT; x++) { a0[x] = u128v{0, 0}; a1[x] = u128v{0, 0}; }
-            for (int j = 0; j < nd; j++) {
-                const u64 k0 = evk[(((size_t)j * 2) * LK + p) * n + i];
-                const u64 k1 = evk[(((size_t)j * 2 + 1) * LK + p) * n + i];
-#pragma unroll
-                for (int x = 0; x < BT; x++) {
-                    if (b0 + x < B) {
-                        const u64 u = ext[(size_t)(b0 + x) * ext_item_stride + (size_t)j * ext_digit_stride +
-                                          (size_t)e * n + i];
-                        acc_wide(a0[x], u, k0);
-                        acc_wide(a1[x], u, k1);
-                    }
-                }
-                if ((j & 3) == 3 && j + 1 < nd) {
-#pragma unroll
-                    for (int x = 0; x < BT; x++) {
-                        a0[x] = u128v{0, barrett128(a0[x], q, r1, r0)};
-                        a1[x] = u128v{0, barrett128(a1[x], q, r1, r0)};
-                    }
-                }
-            }
-#pragma unroll
-            for (int x = 0; x < BT; x++) {
-                if (b0 + x < B) {
-                    u64* ap = acc + (size_t)(b0 + x) * acc_item_stride;
-                    ap[(size_t)e * n + i] = barrett128(a0[x], q, r1, r0);
-                    ap[((size_t)(nl + K) + e) * n + i] = barrett128(a1[x], q, r1, r0);
-                }
-            }
+    u128v a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
+    const u64* xb = ext + (size_t)b * ext_item_stride + (size_t)e * n + i;
+    for (int j = 0; j < nd; j++) {
+        const ulonglong2 k0 = ld2(evk + (((size_t)j * 2) * LK + p) * n + i);
+        const ulonglong2 k1 = ld2(evk + (((size_t)j * 2 + 1) * LK + p) * n + i);
+        const ulonglong2 u = ld2(xb + (size_t)j * ext_digit_stride);
+        acc_wide(a00, u.x, k0.x);
+        acc_wide(a01, u.y, k0.y);
+        acc_wide(a10, u.x, k1.x);
+        acc_wide(a11, u.y, k1.y);
+        if ((j & 3) == 3 && j + 1 < nd) {
+            a00 = u128v{0, barrett128(a00, q, r1, r0)};
+            a01 = u128v{0, barrett128(a01, q, r1, r0)};
+            a10 = u128v{0, barrett128(a10, q, r1, r0)};
+            a11 = u128v{0, barrett128(a11, q, r1, r0)};
         }
     }
+    u64* ap = acc + (size_t)b * acc_item_stride;
+    st2(ap + (size_t)e * n + i, barrett128(a00, q, r1, r0), barrett128(a01, q, r1, r0));
+    st2(ap + ((size_t)(nl + K) + e) * n + i, barrett128(a10, q, r1, r0), barrett128(a11, q, r1, r0));
 }
 
 // ModDown conversion: mdc[b][poly][i] = sum_k [a_k * phinv_k]_{p_k} * phmod[k][i] mod q_i
 // Centred conversion (see oracle oc_moddown_convert): subtract r*P with
 // r = round(sum_k y_k / p_k) evaluated in IEEE double without contraction,
 // so the ModDown error is the zero-mean rounding of x / P.
+template <int MK>
 __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n,
                                int nl, int K, int L, const u64* phinv, const u64* phinv_sh, const u64* phm,
                                const u64* phms, const u64* pinv_dbl, const u64* pm, const u64* pm_sh, Tables tb) {
@@ -573,22 +584,37 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
     const int ne = nl + K;
     const u64* ap = acc + (size_t)b * acc_item_stride + (size_t)poly * ne * n;
     u64* mp = mdc + (size_t)b * mdc_item_stride + (size_t)poly * L * n;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        u64 z[HELR_MAXP];
-        double v = 0.0;
-        for (int k = 0; k < K; k++) {
+    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= n) return;
+    u64 z0[MK], z1[MK];
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < MK; k++) {
+        if (k < K) {
             const u64 pk = tb.q[L + k];
-            z[k] = shoup(ap[(size_t)(nl + k) * n + i], phinv[k], phinv_sh[k], pk);
-            v = __dadd_rn(v, __dmul_rn(__ull2double_rn(z[k]), __longlong_as_double((long long)pinv_dbl[k])));
+            const double inv = __longlong_as_double((long long)pinv_dbl[k]);
+            const ulonglong2 x = ld2(ap + (size_t)(nl + k) * n + i);
+            z0[k] = shoup(x.x, phinv[k], phinv_sh[k], pk);
+            z1[k] = shoup(x.y, phinv[k], phinv_sh[k], pk);
+            v0 = __dadd_rn(v0, __dmul_rn(__ull2double_rn(z0[k]), inv));
+            v1 = __dadd_rn(v1, __dmul_rn(__ull2double_rn(z1[k]), inv));
         }
-        const u64 r = (u64)__double2ull_rd(__dadd_rn(v, 0.5));
-        for (int p = 0; p < nl; p++) {
-            const u64 q = tb.q[p];
-            u64 s = 0;
-            for (int k = 0; k < K; k++)
-                s = add_mod(s, shoup(z[k], phm[(size_t)k * L + p], phms[(size_t)k * L + p], q), q);
-            mp[(size_t)p * n + i] = sub_mod(s, shoup(r, pm[p], pm_sh[p], q), q);
+    }
+    const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
+    const u64 rr1 = (u64)__double2ull_rd(__dadd_rn(v1, 0.5));
+    for (int p = 0; p < nl; p++) {
+        const u64 q = tb.q[p];
+        u64 s0 = 0, s1 = 0;
+#pragma unroll
+        for (int k = 0; k < MK; k++) {
+            if (k < K) {
+                const u64 w = phm[(size_t)k * L + p], ws = phms[(size_t)k * L + p];
+                s0 = add_mod(s0, shoup(z0[k], w, ws, q), q);
+                s1 = add_mod(s1, shoup(z1[k], w, ws, q), q);
+            }
         }
+        st2(mp + (size_t)p * n + i, sub_mod(s0, shoup(rr0, pm[p], pm_sh[p], q), q),
+            sub_mod(s1, shoup(rr1, pm[p], pm_sh[p], q), q));
     }
 }
 
@@ -599,17 +625,25 @@ __global__ void k_moddown_final(const u64* acc, long long acc_item_stride, const
     const int it = blockIdx.z, b = it >> 1, poly = it & 1;
     const int ne = nl + K;
     const u64 q = tb.q[p];
+    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= n) return;
     const u64* ap = acc + (size_t)b * acc_item_stride + ((size_t)poly * ne + p) * n;
     const u64* mp = mdc + (size_t)b * mdc_item_stride + ((size_t)poly * L + p) * n;
     u64* op = ep.out + (size_t)b * ep.out_stride + ((size_t)poly * L + p) * n;
-    const u64* aa = ep.add_a ? ep.add_a + (size_t)b * ep.add_a_stride + ((size_t)poly * L + p) * n : nullptr;
-    const u64* pp = (ep.add_p && poly == 0) ? ep.add_p + (size_t)b * ep.add_p_stride + (size_t)p * n : nullptr;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        u64 v = shoup(sub_mod(ap[i], mp[i], q), pinv[p], pinv_sh[p], q);
-        if (aa) v = add_mod(v, aa[i], q);
-        if (pp) v = add_mod(v, pp[galois_perm(i, (u64)ep.galois, log_n)], q);
-        op[i] = v;
+    const ulonglong2 x = ld2(ap + i), c = ld2(mp + i);
+    u64 v0 = shoup(sub_mod(x.x, c.x, q), pinv[p], pinv_sh[p], q);
+    u64 v1 = shoup(sub_mod(x.y, c.y, q), pinv[p], pinv_sh[p], q);
+    if (ep.add_a) {
+        const ulonglong2 y = ld2(ep.add_a + (size_t)b * ep.add_a_stride + ((size_t)poly * L + p) * n + i);
+        v0 = add_mod(v0, y.x, q);
+        v1 = add_mod(v1, y.y, q);
     }
+    if (ep.add_p && poly == 0) {
+        const u64* pp = ep.add_p + (size_t)b * ep.add_p_stride + (size_t)p * n;
+        v0 = add_mod(v0, pp[galois_perm(i, (u64)ep.galois, log_n)], q);
+        v1 = add_mod(v1, pp[galois_perm(i + 1, (u64)ep.galois, log_n)], q);
+    }
+    st2(op + i, v0, v1);
 }
 
 // Loader applying the Galois permutation to a plain buffer (rotation input).
@@ -665,9 +699,11 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
     {
         ModUpArgs a{w.coef, w.coef_s, in.d, in.d_stride, in.galois, w.ext, w.ext_s, w.ext_ds, c->d_tab, c->d_modup_offs + (size_t)level * c->beta,
                     n, c->log_n, nl, K, L, c->alpha};
-        dim3 g(blocks_for(n, 128) < 64 ? blocks_for(n, 128) : 64, nd, B);
+        dim3 g(blocks_for(n / 2, 128), nd, B);
         ProfScope ps(PROF_MODUP, 8.0 * n * B * (2.0 * nl + (double)nd * ne), s);
-        k_modup<<<g, 128, 0, s>>>(a, c->t);
+        if (c->alpha <= 4) k_modup<4><<<g, 128, 0, s>>>(a, c->t);
+        else if (c->alpha <= 8) k_modup<8><<<g, 128, 0, s>>>(a, c->t);
+        else k_modup<HELR_MAXP><<<g, 128, 0, s>>>(a, c->t);
         CHECK_KERNEL("ks modup");
     }
     // 3) NTT of every converted limb of every digit (one launch per 128 limbs)
@@ -691,9 +727,11 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
     }
     // 4) inner product with the key
     {
-        dim3 g(blocks_for(n, 256) < 32 ? blocks_for(n, 256) : 32, ne);
+        const int by = B < 8 ? B : 8;
+        dim3 g(blocks_for(n / 2, 64), ne, (B + by - 1) / by);
         ProfScope ps(PROF_INNER, 8.0 * n * ((double)B * nd * ne + 2.0 * nd * ne + 2.0 * B * ne), s);
-        k_ks_inner<4><<<g, 256, 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B, c->t);
+        k_ks_inner<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B,
+                                              c->t);
         CHECK_KERNEL("ks inner");
     }
     // 5) ModDown: INTT of the P limbs (both polys), conversion, NTT, combine
@@ -707,10 +745,11 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
             }
         ntt_buffers<true>(c, w.acc, w.acc_s, w.acc, w.acc_s, m, B, s);
         CHECK_LAUNCH("ks moddown intt");
-        dim3 g(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, 2 * B);
+        dim3 g(blocks_for(n / 2, 128), 2 * B);
         {
             ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + nl), s);
-            k_moddown_conv<<<g, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv, c->md_phinv_sh,
+            auto conv = K <= 4 ? k_moddown_conv<4> : (K <= 8 ? k_moddown_conv<8> : k_moddown_conv<HELR_MAXP>);
+            conv<<<g, 128, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv, c->md_phinv_sh,
                                              c->md_phmod, c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
             CHECK_KERNEL("ks moddown conv");
         }
@@ -723,7 +762,7 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
             }
         ntt_buffers<false>(c, w.mdc, w.mdc_s, w.mdc, w.mdc_s, mq, B, s);
         CHECK_LAUNCH("ks moddown ntt");
-        dim3 g2(blocks_for(n, 256) < 64 ? blocks_for(n, 256) : 64, nl, 2 * B);
+        dim3 g2(blocks_for(n / 2, 256), nl, 2 * B);
         {
             ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * nl * (3.0 + (ep.add_a ? 1 : 0) + (ep.add_p ? 0.5 : 0)), s);
             k_moddown_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, ep, n, c->log_n, nl, K, L, c->md_pinv,
@@ -777,7 +816,7 @@ int op_mul_relin_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, 
     for (int b0 = 0; b0 < count; b0 += chunk) {
         int nb = count - b0 < chunk ? count - b0 : chunk;
         KsWs w = ks_ws(c, chunk);
-        dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, nb);
+        dim3 g(blocks_for(c->n, 256), level + 1, nb);
         TensorArgs ta{a + (size_t)b0 * a_is, a_is, a_ts, b + (size_t)b0 * b_is, b_is, b_ts, terms};
         {
             ProfScope ps(PROF_TENSOR, 8.0 * c->n * nb * (level + 1) * (4.0 * terms + 3.0), s);
@@ -858,7 +897,7 @@ int op_lincomb(helr_ctx* c, int terms, const u64* const* x, const long long* xs,
         la.k[t] = t < terms ? k[t] : nullptr;
     }
     la.terms = terms;
-    dim3 g(blocks_for(c->n, 256) < 64 ? blocks_for(c->n, 256) : 64, level + 1, 2 * count);
+    dim3 g(blocks_for(c->n, 256), level + 1, 2 * count);
     ProfScope ps(PROF_ELEM, 8.0 * c->n * 2.0 * count * (level + 1) * (terms + 1), s);
     k_lincomb<<<g, 256, 0, s>>>(la, out, os, c->n, c->L, c->t);
     CHECK_KERNEL("lincomb");
