@@ -130,6 +130,17 @@ int helr_rotate(helr_ctx* ctx, const uint64_t* a, int64_t galois,
                 const uint64_t* gk, uint64_t* out, int count, int level,
                 int accumulate, void* stream);
 
+/* Hoisted rotate-and-sum: out = [a +] sum_{t<nsteps} rot_{galois[t]}(a)
+ * (include_identity selects the a term).  One ModUp of c1, the inner
+ * products of all rotations summed in the extended basis, one ModDown
+ * ("double hoisting").  A baby-step/giant-step pair of calls computes
+ * sum_{k<g} rot_k(a), i.e. each half of sum_col_vec (hesim.py:255-264)
+ * with ~4x fewer NTTs than log2(g) sequential rotate-and-add steps.
+ * galois: host array; keys: host array of device key pointers; nsteps <= 32. */
+int helr_rotsum(helr_ctx* ctx, const uint64_t* a, int nsteps, const int64_t* galois,
+                const uint64_t* const* keys, uint64_t* out, int count, int level,
+                int include_identity, void* stream);
+
 /* ---- refresh stand-in (SimContext.bootstrap, hesim.py:228-236) ---------- */
 
 /* NOT bootstrapping: decrypts through q_0 with the secret key, multiplies the
@@ -174,6 +185,11 @@ typedef struct helr_nag_args {
     int phase;  /* 0: full mini-batch iteration; 1: grad = this batch's gradient;
                    2: grad += this batch's gradient; 3: finish from grad (row sums,
                    Bbar product, update) */
+    int log_baby; /* 0: sum_col_vec by log2(g) rotate-and-add steps (rot_left[i] /
+                     rot_right[i] rotate by 2^i); bs > 0: baby-step/giant-step with
+                     two hoisted groups per half, rot_left = keys for rotations
+                     1..2^bs-1 then 2^bs*(1..2^(log_g-bs)-1), rot_right likewise
+                     for the negated steps */
 } helr_nag_args;
 
 int helr_nag_iteration(helr_ctx* ctx, const helr_nag_args* args, void* stream);

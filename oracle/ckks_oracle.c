@@ -494,21 +494,17 @@ void oc_moddown_convert(oc_ctx* c, const u64* in, u64* out, int nl) {
 /* ---------------- key switching ----------------
  * d: NTT-form limbs 0..level of one polynomial (limb stride N).
  * evk: u64[beta][2][L+K][N].  k0, k1: outputs, limbs 0..level (stride N). */
-void oc_keyswitch(oc_ctx* c, const u64* d, const u64* evk, int level, u64* k0, u64* k1) {
-    int N = c->n, L = c->L, K = c->K, LK = L + K, al = c->alpha;
-    int nl = level + 1;              /* Q limbs in use */
-    int ext = nl + K;                /* extended basis size */
-    int nd = (nl + al - 1) / al;     /* digits in use */
-    int idx[MAXP];                   /* extended limb -> prime index */
+/* ModUp of d (NTT form, limbs 0..level) into up[nd][ext][N]: per digit, the
+ * digit's own limbs copied, the others by fast basis conversion + NTT. */
+static void modup_all(oc_ctx* c, const u64* d, int level, u64* up) {
+    int N = c->n, L = c->L, K = c->K, al = c->alpha;
+    int nl = level + 1, ext = nl + K, nd = (nl + al - 1) / al;
+    int idx[MAXP];
     for (int i = 0; i < nl; i++) idx[i] = i;
     for (int k = 0; k < K; k++) idx[nl + k] = L + k;
-
     u64* coef = (u64*)malloc(sizeof(u64) * (size_t)nl * N);
     memcpy(coef, d, sizeof(u64) * (size_t)nl * N);
     for (int i = 0; i < nl; i++) oc_intt(c, coef + (size_t)i * N, i);
-
-    u64* acc = (u64*)calloc((size_t)2 * ext * N, sizeof(u64));
-    u64* up = (u64*)malloc(sizeof(u64) * (size_t)ext * N);
     for (int j = 0; j < nd; j++) {
         int lo = j * al, hi = lo + al < nl ? lo + al : nl;
         int src[MAXP], dst[MAXP], ns = hi - lo, ndst = 0;
@@ -519,7 +515,7 @@ void oc_keyswitch(oc_ctx* c, const u64* d, const u64* evk, int level, u64* k0, u
         oc_basis_convert(c, coef + (size_t)lo * N, src, ns, conv, dst, ndst);
         int w = 0;
         for (int e = 0; e < ext; e++) {
-            u64* u = up + (size_t)e * N;
+            u64* u = up + ((size_t)j * ext + e) * N;
             if (e >= lo && e < hi) {
                 memcpy(u, d + (size_t)e * N, sizeof(u64) * N);
             } else {
@@ -529,23 +525,38 @@ void oc_keyswitch(oc_ctx* c, const u64* d, const u64* evk, int level, u64* k0, u
             }
         }
         free(conv);
-        for (int b = 0; b < 2; b++)
-            for (int e = 0; e < ext; e++) {
-                int p = idx[e];
-                u64 q = c->prm[p];
+    }
+    free(coef);
+}
+
+/* acc[b][ext][N] += sum_j up_j (.) evk_j[b]   (optionally up_j permuted by galois) */
+static void inner_acc(oc_ctx* c, const u64* up, const u64* evk, int level, u64 galois, u64* acc) {
+    int N = c->n, L = c->L, K = c->K, LK = L + K, al = c->alpha;
+    int nl = level + 1, ext = nl + K, nd = (nl + al - 1) / al;
+    u64* tmp = (u64*)malloc(sizeof(u64) * N);
+    for (int j = 0; j < nd; j++)
+        for (int e = 0; e < ext; e++) {
+            int p = e < nl ? e : L + (e - nl);
+            u64 q = c->prm[p];
+            const u64* u = up + ((size_t)j * ext + e) * N;
+            if (galois) { automorph_poly(c, u, tmp, galois); u = tmp; }
+            for (int b = 0; b < 2; b++) {
                 const u64* kk = evk + ((size_t)(j * 2 + b) * LK + p) * N;
                 u64* a = acc + ((size_t)b * ext + e) * N;
-                const u64* u = up + (size_t)e * N;
                 for (int i = 0; i < N; i++) a[i] = addm(a[i], mulm(u[i], kk[i], q), q);
             }
-    }
-    free(up);
-    free(coef);
-    /* ModDown */
+        }
+    free(tmp);
+}
+
+/* ModDown of acc[2][ext][N] (centred) into k0, k1 (limbs 0..level) */
+static void moddown_both(oc_ctx* c, const u64* acc, int level, u64* k0, u64* k1) {
+    int N = c->n, L = c->L, K = c->K;
+    int nl = level + 1, ext = nl + K;
     u64* pc = (u64*)malloc(sizeof(u64) * (size_t)K * N);
     u64* conv = (u64*)malloc(sizeof(u64) * (size_t)nl * N);
     for (int b = 0; b < 2; b++) {
-        u64* a = acc + (size_t)b * ext * N;
+        const u64* a = acc + (size_t)b * ext * N;
         memcpy(pc, a + (size_t)nl * N, sizeof(u64) * (size_t)K * N);
         for (int k = 0; k < K; k++) oc_intt(c, pc + (size_t)k * N, L + k);
         oc_moddown_convert(c, pc, conv, nl);
@@ -560,7 +571,57 @@ void oc_keyswitch(oc_ctx* c, const u64* d, const u64* evk, int level, u64* k0, u
             for (int n = 0; n < N; n++) o[n] = mulm(subm(x[n], t[n], q), pinv, q);
         }
     }
-    free(pc); free(conv); free(acc);
+    free(pc); free(conv);
+}
+
+/* d: NTT-form limbs 0..level of one polynomial (limb stride N).
+ * evk: u64[beta][2][L+K][N].  k0, k1: outputs, limbs 0..level (stride N). */
+void oc_keyswitch(oc_ctx* c, const u64* d, const u64* evk, int level, u64* k0, u64* k1) {
+    int N = c->n, K = c->K, al = c->alpha;
+    int nl = level + 1, ext = nl + K, nd = (nl + al - 1) / al;
+    u64* up = (u64*)malloc(sizeof(u64) * (size_t)nd * ext * N);
+    u64* acc = (u64*)calloc((size_t)2 * ext * N, sizeof(u64));
+    modup_all(c, d, level, up);
+    inner_acc(c, up, evk, level, 0, acc);
+    moddown_both(c, acc, level, k0, k1);
+    free(up); free(acc);
+}
+
+/* Hoisted rotate-and-sum (device helr_rotsum): out = [a +] sum_t rot_{g_t}(a)
+ * with one ModUp of c1, sigma_t applied to the ModUp'd digits, the inner
+ * products summed in the extended basis and one ModDown. */
+void oc_rotsum(oc_ctx* c, const u64* a, int nsteps, const int64_t* gal, const u64* const* keys, u64* out, int count,
+               int level, int include_identity) {
+    int N = c->n, L = c->L, K = c->K, al = c->alpha;
+    int nl = level + 1, ext = nl + K, nd = (nl + al - 1) / al;
+#pragma omp parallel for
+    for (int x = 0; x < count; x++) {
+        const u64* ax = a + (size_t)x * 2 * L * N;
+        u64* ox = out + (size_t)x * 2 * L * N;
+        u64* up = (u64*)malloc(sizeof(u64) * (size_t)nd * ext * N);
+        u64* acc = (u64*)calloc((size_t)2 * ext * N, sizeof(u64));
+        u64* k0 = (u64*)malloc(sizeof(u64) * (size_t)nl * N);
+        u64* k1 = (u64*)malloc(sizeof(u64) * (size_t)nl * N);
+        u64* tmp = (u64*)malloc(sizeof(u64) * N);
+        modup_all(c, ax + (size_t)L * N, level, up);
+        for (int t = 0; t < nsteps; t++) inner_acc(c, up, keys[t], level, (u64)gal[t], acc);
+        moddown_both(c, acc, level, k0, k1);
+        for (int p = 0; p < nl; p++) {
+            u64 q = c->prm[p];
+            const u64 *a0 = ax + (size_t)p * N, *a1 = ax + ((size_t)L + p) * N;
+            u64 *o0 = ox + (size_t)p * N, *o1 = ox + ((size_t)L + p) * N;
+            for (int i = 0; i < N; i++) {
+                o0[i] = k0[(size_t)p * N + i];
+                o1[i] = k1[(size_t)p * N + i];
+                if (include_identity) { o0[i] = addm(o0[i], a0[i], q); o1[i] = addm(o1[i], a1[i], q); }
+            }
+            for (int t = 0; t < nsteps; t++) {
+                automorph_poly(c, a0, tmp, (u64)gal[t]);
+                for (int i = 0; i < N; i++) o0[i] = addm(o0[i], tmp[i], q);
+            }
+        }
+        free(up); free(acc); free(k0); free(k1); free(tmp);
+    }
 }
 
 /* tensor of one pair: d = [d0, d1, d2] (u64[3][L][N]) for limbs 0..level */

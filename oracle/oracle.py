@@ -65,6 +65,8 @@ def lib():
             "oc_rescale": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_int]),
             "oc_basis_convert": (None, [vp, _u64p, _intp, ctypes.c_int, _u64p, _intp, ctypes.c_int]),
             "oc_keyswitch": (None, [vp, _u64p, _u64p, ctypes.c_int, _u64p, _u64p]),
+            "oc_rotsum": (None, [vp, _u64p, ctypes.c_int, _i64p, ctypes.POINTER(_u64p), _u64p, ctypes.c_int,
+                                 ctypes.c_int, ctypes.c_int]),
             "oc_tensor": (None, [vp, _u64p, _u64p, _u64p, ctypes.c_int]),
             "oc_mul_relin": (None, [vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_int, ctypes.c_int]),
             "oc_automorph": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
@@ -241,6 +243,16 @@ class Oracle:
     def rotate(self, a, galois, gk, level, accumulate=False):
         out = self._out(a)
         lib().oc_rotate(self._h, _p(a), galois, _p(gk), _p(out), a.shape[0], level, 1 if accumulate else 0)
+        return out
+
+    def rotsum(self, a, gals, keys, level, include_identity=True):
+        """[a +] sum_t rot_{gals[t]}(a) with one hoisted key switch."""
+        a = np.ascontiguousarray(a)
+        out = self._out(a)
+        g = np.ascontiguousarray(np.array(gals, dtype=np.int64))
+        ks = [np.ascontiguousarray(k) for k in keys]
+        arr = (_u64p * len(ks))(*[_p(k) for k in ks])
+        lib().oc_rotsum(self._h, _p(a), len(ks), _p(g), arr, _p(out), a.shape[0], level, 1 if include_identity else 0)
         return out
 
     def refresh(self, sk, a, in_level, ratio, out_level, seed, first_id):

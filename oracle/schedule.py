@@ -54,7 +54,22 @@ def _lincomb(orc, terms, level):
     return acc
 
 
-def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, log_m, phase=0, grad=None):
+def _bsgs(orc, x, gkeys, log_g, bs, sign, level):
+    """sum_{k < 2^log_g} rot(x, sign k) as two hoisted groups (helr_rotsum):
+    baby steps 1..2^bs-1, then giant steps 2^bs (1..2^gs-1)."""
+    N = orc.N
+    bs = min(bs, log_g)
+    gs = log_g - bs
+    baby = [_galois(sign * k, N) for k in range(1, 1 << bs)]
+    x = orc.rotsum(np.ascontiguousarray(x), baby, [gkeys[g] for g in baby], level, include_identity=True)
+    if gs:
+        giant = [_galois(sign * (k << bs), N) for k in range(1, 1 << gs)]
+        x = orc.rotsum(x, giant, [gkeys[g] for g in giant], level, include_identity=True)
+    return x
+
+
+def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, log_m, phase=0, grad=None,
+                  log_baby=0):
     """z: u64[R][C][2][L][N]; w, v, bbar, grad: u64[C][2][L][N];
     gkeys: galois element -> key; consts: u64[10][L].
     Returns (w', v') for phase 0, the gradient for phases 1/2, (w', v') for 3."""
@@ -70,15 +85,21 @@ def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, lo
             prod = _tensor_sum_relin(orc, [(z[r, j][None], w[j][None]) for j in range(C)], rlk, lw)
             x = orc.rescale(prod, lw)
             # sum_col_vec left half (hesim.py:255-257)
-            for i in range(log_g):
-                ge = _galois(1 << i, N)
-                x = orc.rotate(x, ge, gkeys[ge], lw - 1, accumulate=True)
+            if log_baby > 0:
+                x = _bsgs(orc, x, gkeys, log_g, log_baby, +1, lw - 1)
+            else:
+                for i in range(log_g):
+                    ge = _galois(1 << i, N)
+                    x = orc.rotate(x, ge, gkeys[ge], lw - 1, accumulate=True)
             # row-start mask (hesim.py:258-260)
             x = orc.rescale(orc.mul_plain(x, mask_pt, lw - 1), lw - 1)
             # right half (hesim.py:262-264)
-            for i in range(log_g):
-                ge = _galois(S - (1 << i), N)
-                x = orc.rotate(x, ge, gkeys[ge], lw - 2, accumulate=True)
+            if log_baby > 0:
+                x = _bsgs(orc, x, gkeys, log_g, log_baby, -1, lw - 2)
+            else:
+                for i in range(log_g):
+                    ge = _galois(S - (1 << i), N)
+                    x = orc.rotate(x, ge, gkeys[ge], lw - 2, accumulate=True)
             u = x
             # complement polynomial q0 + q1 u + q2 u^2 + q3 u^3 (enctrain.py:186-191)
             u2 = orc.rescale(orc.mul_relin(u, u, rlk, lw - 2), lw - 2)

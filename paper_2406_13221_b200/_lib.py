@@ -52,6 +52,8 @@ SIGNATURES = {
     "helr_imul": [_vp, _u64p, _u64p, _i, _i, _vp],
     "helr_rotate": [_vp, _u64p, _i64, _u64p, _u64p, _i, _i, _i, _vp],
     "helr_refresh": [_vp, _u64p, _u64p, _i, ctypes.c_double, _u64p, _i, _i, _u64, _u64, _vp],
+    "helr_rotsum": [_vp, _u64p, _i, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p), _u64p, _i, _i, _i,
+                    _vp],
     "helr_nag_iteration": None,  # bound lazily by driver.py (struct argument)
     "helr_last_error": [ctypes.c_char_p, ctypes.c_size_t],
     "helr_version": [],

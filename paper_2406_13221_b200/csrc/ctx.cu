@@ -132,9 +132,17 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
     size_t o_tw = put(2 * (size_t)LK * n);
     size_t o_itw = put(2 * (size_t)LK * n);
     size_t o_ni = put(LK), o_nis = put(LK), o_i1 = put(LK), o_i1s = put(LK);
+    size_t o_one = put(LK), o_t128 = put(LK), o_t128s = put(LK);  // floor(2^64/q); 2^128 mod q (+ Shoup)
     for (int p = 0; p < LK; p++) {
         u64 q = primes[p];
         h[o_q + p] = q;
+        h[o_one + p] = hshoup(1, q);
+        {
+            u64 t64 = (u64)(((h128)1 << 64) % q);
+            u64 t = hmul(t64, t64, q);
+            h[o_t128 + p] = t;
+            h[o_t128s + p] = hshoup(t, q);
+        }
         h128 ratio = (~(h128)0) / q;  // floor((2^128 - 1)/q) == floor(2^128/q) for odd q
         h[o_b1 + p] = (u64)(ratio >> 64);
         h[o_b0 + p] = (u64)ratio;
@@ -227,6 +235,7 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
     c->md_phmod = d + o_phm; c->md_phmod_sh = d + o_phms;
     c->md_pinv = d + o_pi; c->md_pinv_sh = d + o_pis; c->pmod = d + o_pm; c->pmod_sh = d + o_pms; c->md_pinv_dbl = d + o_pid;
     c->imul_f = d + o_im;
+    c->one_sh = d + o_one; c->t128 = d + o_t128; c->t128_sh = d + o_t128s;
     c->modup = d;  // offsets in modup_off are absolute word offsets into d_tab
 
     if (!cuda_ok(cudaMalloc(&c->d_modup_offs, c->modup_off.size() * sizeof(size_t)), "cudaMalloc(offsets)") ||

@@ -57,6 +57,9 @@ struct helr_ctx {
     const u64* pmod_sh = nullptr;
     const u64* md_pinv_dbl = nullptr;  // [K] bits of (double)1/p_k
     const u64* imul_f = nullptr;       // [L][N] NTT of X^(N/2)
+    const u64* one_sh = nullptr;       // [LK] floor(2^64 / q)
+    const u64* t128 = nullptr;         // [LK] 2^128 mod q
+    const u64* t128_sh = nullptr;
     // key-switching workspace
     u64* ws = nullptr;
     size_t ws_words = 0;

@@ -60,6 +60,29 @@ static long long pow_mod_ll(long long b, long long e, long long m) {
     return r;
 }
 
+// sum_{k < 2^log_g} rot(x, sign*k) by baby-step/giant-step: two hoisted
+// rotate-and-sum groups (baby 1..2^bs-1, giant 2^bs*(1..2^gs-1)), each with one
+// ModUp and one ModDown.  keys: baby keys then giant keys.  `in` is clobbered
+// as scratch; the result lands in `out`.
+static int bsgs_rotsum(helr_ctx* c, const uint64_t* const* keys, int log_g, int bs, int sign, u64* in, u64* out, int R,
+                       int level, cudaStream_t s) {
+    const long long CS = 2ll * c->L * c->n, two_n = 2ll * c->n, slots = c->n / 2;
+    if (bs > log_g) bs = log_g;
+    const int gs = log_g - bs;
+    const int nb = (1 << bs) - 1, ng = (1 << gs) - 1;
+    long long gal[64];
+    for (int k = 1; k <= nb; k++) gal[k - 1] = pow_mod_ll(5, sign > 0 ? k : slots - k, two_n);
+    if (ng == 0) return op_rotsum_hoisted(c, in, CS, nb, gal, (const u64* const*)keys, out, CS, R, level, 1, s);
+    TRY(op_rotsum_hoisted(c, in, CS, nb, gal, (const u64* const*)keys, out, CS, R, level, 1, s));
+    for (int k = 1; k <= ng; k++) {
+        const long long step = (long long)k << bs;
+        gal[k - 1] = pow_mod_ll(5, sign > 0 ? step : slots - step, two_n);
+    }
+    TRY(op_rotsum_hoisted(c, out, CS, ng, gal, (const u64* const*)(keys + nb), in, CS, R, level, 1, s));
+    cudaMemcpyAsync(out, in, (size_t)R * CS * sizeof(u64), cudaMemcpyDeviceToDevice, s);
+    return HELR_OK;
+}
+
 static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
     const int L = c->L, n = c->n;
     const long long CS = 2ll * L * n;
@@ -91,26 +114,35 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
         // 1) P_r = relin(sum_j Z_rj (x) W_j), rescale -> lw-1
         TRY(op_mul_relin_sum(c, a->z, (long long)C * CS, CS, a->w, 0, CS, C, a->rlk, T1, CS, R, lw, s));
         TRY(op_rescale(c, T1, CS, X0, CS, R, lw, s));
-        // 2) rotate-and-add left by 1, 2, ..., g/2 (sum_col_vec, hesim.py:255-257)
+        // 2) sum_{k<g} rot(P, k): the left half of sum_col_vec (hesim.py:255-257)
         u64* cur = X0;
         u64* nxt = X1;
-        for (int i = 0; i < a->log_g; i++) {
-            const long long g = pow_mod_ll(5, 1ll << i, two_n);
-            TRY(op_rotate(c, cur, CS, g, a->rot_left[i], nxt, CS, R, lw - 1, 1, s));
+        if (a->log_baby > 0) {
+            TRY(bsgs_rotsum(c, a->rot_left, a->log_g, a->log_baby, +1, cur, nxt, R, lw - 1, s));
             u64* t = cur; cur = nxt; nxt = t;
+        } else {
+            for (int i = 0; i < a->log_g; i++) {
+                const long long g = pow_mod_ll(5, 1ll << i, two_n);
+                TRY(op_rotate(c, cur, CS, g, a->rot_left[i], nxt, CS, R, lw - 1, 1, s));
+                u64* t = cur; cur = nxt; nxt = t;
+            }
         }
         // 3) row-start mask (hesim.py:258-260), rescale -> lw-2
         TRY(op_ew(c, EW_MULPT, cur, CS, a->mask_pt, 0, T1, CS, R, lw - 1, s));
         TRY(op_rescale(c, T1, CS, cur, CS, R, lw - 1, s));
-        // 4) rotate-and-add right by 1, ..., g/2 (hesim.py:262-264)
-        for (int i = 0; i < a->log_g; i++) {
-            const long long g = pow_mod_ll(5, slots - (1ll << i), two_n);
-            u64* dst = (i == a->log_g - 1) ? U : nxt;
-            TRY(op_rotate(c, cur, CS, g, a->rot_right[i], dst, CS, R, lw - 2, 1, s));
-            u64* t = cur; cur = dst; nxt = t;
-        }
-        if (a->log_g == 0) {
-            cudaMemcpyAsync(U, cur, (size_t)R * CS * sizeof(u64), cudaMemcpyDeviceToDevice, s);
+        // 4) sum_{k<g} rot(M, -k): the right half (hesim.py:262-264)
+        if (a->log_baby > 0) {
+            TRY(bsgs_rotsum(c, a->rot_right, a->log_g, a->log_baby, -1, cur, U, R, lw - 2, s));
+        } else {
+            for (int i = 0; i < a->log_g; i++) {
+                const long long g = pow_mod_ll(5, slots - (1ll << i), two_n);
+                u64* dst = (i == a->log_g - 1) ? U : nxt;
+                TRY(op_rotate(c, cur, CS, g, a->rot_right[i], dst, CS, R, lw - 2, 1, s));
+                u64* t = cur; cur = dst; nxt = t;
+            }
+            if (a->log_g == 0) {
+                cudaMemcpyAsync(U, cur, (size_t)R * CS * sizeof(u64), cudaMemcpyDeviceToDevice, s);
+            }
         }
         // 5) u^2 (lw-3)
         TRY(op_mul_relin_sum(c, U, CS, 0, U, CS, 0, 1, a->rlk, T1, CS, R, lw - 2, s));

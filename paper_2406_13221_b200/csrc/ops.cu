@@ -456,15 +456,25 @@ struct KsInput {
     long long d_stride;
     long long galois;    // 0: none, else apply X -> X^galois to d first
 };
+#define HELR_MAX_HOIST 32
 struct KsEpilogue {
     u64* out;             // ciphertext of item b at out + b*out_stride
     long long out_stride;
     const u64* add_a;     // optional ciphertext-like addend (both polys), stride add_a_stride
     long long add_a_stride;
-    const u64* add_p;     // optional: poly 0 of add_p permuted by galois, added to out poly 0
+    const u64* add_p;     // optional: sum_t sigma_t(poly 0 of add_p) added to out poly 0
     long long add_p_stride;
-    long long galois;
+    int ngal;
+    long long gal[HELR_MAX_HOIST];
 };
+static KsEpilogue make_epilogue(u64* out, long long os, const u64* add_a, long long as, const u64* add_p, long long ps,
+                                int ngal, const long long* gal) {
+    KsEpilogue e;
+    e.out = out; e.out_stride = os; e.add_a = add_a; e.add_a_stride = as; e.add_p = add_p; e.add_p_stride = ps;
+    e.ngal = ngal;
+    for (int t = 0; t < HELR_MAX_HOIST; t++) e.gal[t] = t < ngal ? gal[t] : 0;
+    return e;
+}
 
 // ModUp conversion for digit j; grid (x: coeff tiles, y: digit, z: item)
 struct ModUpArgs {
@@ -640,8 +650,10 @@ __global__ void k_moddown_final(const u64* acc, long long acc_item_stride, const
     }
     if (ep.add_p && poly == 0) {
         const u64* pp = ep.add_p + (size_t)b * ep.add_p_stride + (size_t)p * n;
-        v0 = add_mod(v0, pp[galois_perm(i, (u64)ep.galois, log_n)], q);
-        v1 = add_mod(v1, pp[galois_perm(i + 1, (u64)ep.galois, log_n)], q);
+        for (int t = 0; t < ep.ngal; t++) {
+            v0 = add_mod(v0, pp[galois_perm(i, (u64)ep.gal[t], log_n)], q);
+            v1 = add_mod(v1, pp[galois_perm(i + 1, (u64)ep.gal[t], log_n)], q);
+        }
     }
     st2(op + i, v0, v1);
 }
@@ -678,8 +690,8 @@ static KsWs ks_ws(helr_ctx* c, int B) {
     return w;
 }
 
-static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, KsEpilogue ep, int B, const KsWs& w,
-                           cudaStream_t s) {
+// ModUp of B inputs into w.ext (NTT form over Q_l + P for every digit)
+static int ks_modup(helr_ctx* c, KsInput in, int level, int B, const KsWs& w, cudaStream_t s) {
     const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
     const int nd = (nl + c->alpha - 1) / c->alpha;
     // 1) coef = INTT(sigma(d))
@@ -697,8 +709,8 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
     }
     // 2) ModUp conversions (+ copy of own-digit NTT limbs)
     {
-        ModUpArgs a{w.coef, w.coef_s, in.d, in.d_stride, in.galois, w.ext, w.ext_s, w.ext_ds, c->d_tab, c->d_modup_offs + (size_t)level * c->beta,
-                    n, c->log_n, nl, K, L, c->alpha};
+        ModUpArgs a{w.coef, w.coef_s, in.d, in.d_stride, in.galois, w.ext, w.ext_s, w.ext_ds, c->d_tab,
+                    c->d_modup_offs + (size_t)level * c->beta, n, c->log_n, nl, K, L, c->alpha};
         dim3 g(blocks_for(n / 2, 128), nd, B);
         ProfScope ps(PROF_MODUP, 8.0 * n * B * (2.0 * nl + (double)nd * ne), s);
         if (c->alpha <= 4) k_modup<4><<<g, 128, 0, s>>>(a, c->t);
@@ -725,7 +737,54 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
         if (m.count) ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s);
         CHECK_LAUNCH("ks modup ntt");
     }
-    // 4) inner product with the key
+    return HELR_OK;
+}
+
+// ModDown of w.acc (both polynomials) and the fused epilogue into ep.out
+static int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const KsWs& w, cudaStream_t s) {
+    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
+    LimbMap m;
+    m.count = 2 * K;  // P limbs of both polynomials in one launch
+    for (int poly = 0; poly < 2; poly++)
+        for (int k = 0; k < K; k++) {
+            m.off[poly * K + k] = (unsigned char)(poly * ne + nl + k);
+            m.prime[poly * K + k] = (unsigned char)(L + k);
+        }
+    ntt_buffers<true>(c, w.acc, w.acc_s, w.acc, w.acc_s, m, B, s);
+    CHECK_LAUNCH("ks moddown intt");
+    dim3 g(blocks_for(n / 2, 128), 2 * B);
+    {
+        ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + nl), s);
+        auto conv = K <= 4 ? k_moddown_conv<4> : (K <= 8 ? k_moddown_conv<8> : k_moddown_conv<HELR_MAXP>);
+        conv<<<g, 128, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv, c->md_phinv_sh, c->md_phmod,
+                               c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
+        CHECK_KERNEL("ks moddown conv");
+    }
+    LimbMap mq;
+    mq.count = 2 * nl;
+    for (int poly = 0; poly < 2; poly++)
+        for (int i = 0; i < nl; i++) {
+            mq.off[poly * nl + i] = (unsigned char)(poly * L + i);
+            mq.prime[poly * nl + i] = (unsigned char)i;
+        }
+    ntt_buffers<false>(c, w.mdc, w.mdc_s, w.mdc, w.mdc_s, mq, B, s);
+    CHECK_LAUNCH("ks moddown ntt");
+    dim3 g2(blocks_for(n / 2, 256), nl, 2 * B);
+    {
+        ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * nl * (3.0 + (ep.add_a ? 1 : 0) + (ep.add_p ? 0.5 * ep.ngal : 0)), s);
+        k_moddown_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, ep, n, c->log_n, nl, K, L, c->md_pinv,
+                                           c->md_pinv_sh, c->t);
+        CHECK_KERNEL("ks moddown final");
+    }
+    return HELR_OK;
+}
+
+static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, const KsEpilogue& ep, int B,
+                           const KsWs& w, cudaStream_t s) {
+    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
+    const int nd = (nl + c->alpha - 1) / c->alpha;
+    int r = ks_modup(c, in, level, B, w, s);
+    if (r) return r;
     {
         const int by = B < 8 ? B : 8;
         dim3 g(blocks_for(n / 2, 64), ne, (B + by - 1) / by);
@@ -734,43 +793,114 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, K
                                               c->t);
         CHECK_KERNEL("ks inner");
     }
-    // 5) ModDown: INTT of the P limbs (both polys), conversion, NTT, combine
-    {
-        LimbMap m;
-        m.count = 2 * K;  // P limbs of both polynomials in one launch
-        for (int poly = 0; poly < 2; poly++)
-            for (int k = 0; k < K; k++) {
-                m.off[poly * K + k] = (unsigned char)(poly * ne + nl + k);
-                m.prime[poly * K + k] = (unsigned char)(L + k);
-            }
-        ntt_buffers<true>(c, w.acc, w.acc_s, w.acc, w.acc_s, m, B, s);
-        CHECK_LAUNCH("ks moddown intt");
-        dim3 g(blocks_for(n / 2, 128), 2 * B);
-        {
-            ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + nl), s);
-            auto conv = K <= 4 ? k_moddown_conv<4> : (K <= 8 ? k_moddown_conv<8> : k_moddown_conv<HELR_MAXP>);
-            conv<<<g, 128, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv, c->md_phinv_sh,
-                                             c->md_phmod, c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
-            CHECK_KERNEL("ks moddown conv");
-        }
-        LimbMap mq;
-        mq.count = 2 * nl;
-        for (int poly = 0; poly < 2; poly++)
-            for (int i = 0; i < nl; i++) {
-                mq.off[poly * nl + i] = (unsigned char)(poly * L + i);
-                mq.prime[poly * nl + i] = (unsigned char)i;
-            }
-        ntt_buffers<false>(c, w.mdc, w.mdc_s, w.mdc, w.mdc_s, mq, B, s);
-        CHECK_LAUNCH("ks moddown ntt");
-        dim3 g2(blocks_for(n / 2, 256), nl, 2 * B);
-        {
-            ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * nl * (3.0 + (ep.add_a ? 1 : 0) + (ep.add_p ? 0.5 : 0)), s);
-            k_moddown_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, ep, n, c->log_n, nl, K, L, c->md_pinv,
-                                               c->md_pinv_sh, c->t);
-            CHECK_KERNEL("ks moddown final");
+    return ks_moddown(c, level, ep, B, w, s);
+}
+
+// ---- hoisted rotate-and-sum ------------------------------------------------
+// out = [a +] sum_t rot_{g_t}(a): ONE ModUp of c1, the inner products of every
+// rotation summed in the extended basis (sigma_t applied to the ModUp'd digits
+// by a warp-coalesced gather: a Galois permutation maps every 32-aligned run of
+// NTT slots onto a 32-aligned run), ONE ModDown; sum_t sigma_t(c0) is gathered
+// in the ModDown epilogue.
+struct HoistKeys {
+    int nsteps;
+    const u64* key[HELR_MAX_HOIST];
+    long long gal[HELR_MAX_HOIST];
+};
+struct u192v { u64 lo, mid, hi; };
+__device__ __forceinline__ void mac192(u192v& a, u64 x, u64 y) {
+    const u64 plo = x * y, phi = __umul64hi(x, y);
+    asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, 0;"
+        : "+l"(a.lo), "+l"(a.mid), "+l"(a.hi)
+        : "l"(plo), "l"(phi));
+}
+// (hi 2^128 + mid 2^64 + lo) mod q
+__device__ __forceinline__ u64 reduce192(const u192v& a, u64 q, u64 r1, u64 r0, u64 one_sh, u64 t128, u64 t128_sh) {
+    const u64 mid = shoup(a.mid, 1, one_sh, q);  // mid mod q
+    u64 r = barrett128(u128v{mid, a.lo}, q, r1, r0);
+    if (a.hi) r = add_mod(r, shoup(a.hi, t128, t128_sh, q), q);
+    return r;
+}
+__global__ void k_ks_inner_hoisted(const u64* ext, long long ext_item_stride, long long ext_digit_stride, HoistKeys hk,
+                                   u64* acc, long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK,
+                                   int nd, int B, Tables tb, const u64* one_sh, const u64* t128, const u64* t128_sh) {
+    const int e = blockIdx.z;
+    const int b = blockIdx.y * blockDim.y + threadIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B || i >= n) return;
+    const int p = e < nl ? e : L + (e - nl);
+    const u64 q = tb.q[p];
+    u192v a0{0, 0, 0}, a1{0, 0, 0};
+    const u64* xb = ext + (size_t)b * ext_item_stride + (size_t)e * n;
+    for (int t = 0; t < hk.nsteps; t++) {
+        const int src = galois_perm(i, (u64)hk.gal[t], log_n);
+        const u64* kt = hk.key[t];
+        for (int j = 0; j < nd; j++) {
+            const u64 u = xb[(size_t)j * ext_digit_stride + src];
+            mac192(a0, u, kt[(((size_t)j * 2) * LK + p) * n + i]);
+            mac192(a1, u, kt[(((size_t)j * 2 + 1) * LK + p) * n + i]);
         }
     }
+    u64* ap = acc + (size_t)b * acc_item_stride;
+    const u64 r1 = tb.br1[p], r0 = tb.br0[p];
+    ap[(size_t)e * n + i] = reduce192(a0, q, r1, r0, one_sh[p], t128[p], t128_sh[p]);
+    ap[((size_t)(nl + K) + e) * n + i] = reduce192(a1, q, r1, r0, one_sh[p], t128[p], t128_sh[p]);
+}
+
+int op_rotsum_hoisted(helr_ctx* c, const u64* a, long long as, int nsteps, const long long* gal, const u64* const* keys,
+                      u64* out, long long os, int count, int level, int include_identity, cudaStream_t s) {
+    if (level < 0 || level >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    if (nsteps < 1 || nsteps > HELR_MAX_HOIST) { set_error("rotsum: 1..32 rotations per hoisted group"); return HELR_EINVAL; }
+    if (a == out) { set_error("rotsum: out must not alias the input"); return HELR_EINVAL; }
+    HoistKeys hk;
+    hk.nsteps = nsteps;
+    long long gg[HELR_MAX_HOIST];
+    for (int t = 0; t < HELR_MAX_HOIST; t++) {
+        if (t < nsteps) {
+            const long long g = gal[t] % (2ll * c->n);
+            if (g <= 0 || (g & 1) == 0) { set_error("galois element must be odd and positive"); return HELR_EINVAL; }
+            hk.key[t] = keys[t];
+            hk.gal[t] = g;
+            gg[t] = g;
+        } else {
+            hk.key[t] = nullptr;
+            hk.gal[t] = 1;
+        }
+    }
+    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
+    const int nd = (nl + c->alpha - 1) / c->alpha;
+    const int chunk = c->max_batch;
+    for (int b0 = 0; b0 < count; b0 += chunk) {
+        const int nb = count - b0 < chunk ? count - b0 : chunk;
+        KsWs w = ks_ws(c, chunk);
+        const u64* ab = a + (size_t)b0 * as;
+        KsInput in{ab + (size_t)L * n, as, 0};
+        int r = ks_modup(c, in, level, nb, w, s);
+        if (r) return r;
+        {
+            const int by = nb < 4 ? nb : 4;
+            dim3 g(blocks_for(n, 64), (nb + by - 1) / by, ne);
+            ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne * nsteps + 2.0 * nd * ne * nsteps + 2.0 * nb * ne), s);
+            k_ks_inner_hoisted<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, hk, w.acc, w.acc_s, n, c->log_n, nl,
+                                                          K, L, c->LK, nd, nb, c->t, c->one_sh, c->t128, c->t128_sh);
+            CHECK_KERNEL("rotsum inner");
+        }
+        KsEpilogue ep = make_epilogue(out + (size_t)b0 * os, os, include_identity ? ab : nullptr, as, ab, as, nsteps, gg);
+        r = ks_moddown(c, level, ep, nb, w, s);
+        if (r) return r;
+    }
     return HELR_OK;
+}
+
+extern "C" int helr_rotsum(helr_ctx* c, const uint64_t* a, int nsteps, const int64_t* galois,
+                           const uint64_t* const* keys, uint64_t* out, int count, int level, int include_identity,
+                           void* s) {
+    clear_stale_error("helr_rotsum");
+    const long long cs = 2ll * c->L * c->n;
+    long long g[HELR_MAX_HOIST];
+    for (int t = 0; t < nsteps && t < HELR_MAX_HOIST; t++) g[t] = (long long)galois[t];
+    return op_rotsum_hoisted(c, (const u64*)a, cs, nsteps, g, (const u64* const*)keys, (u64*)out, cs, count, level,
+                             include_identity, S(s));
 }
 
 // tensor sum: d = sum_t a_t (x) b_t  (d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1) into [B][3][L][N]
@@ -825,7 +955,7 @@ int op_mul_relin_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, 
         }
         const long long ts = 3ll * c->L * c->n;
         KsInput in{w.tensor + 2ll * c->L * c->n, ts, 0};
-        KsEpilogue ep{out + (size_t)b0 * os, os, w.tensor, ts, nullptr, 0, 0};
+        KsEpilogue ep = make_epilogue(out + (size_t)b0 * os, os, w.tensor, ts, nullptr, 0, 0, nullptr);
         int r = keyswitch_batch(c, in, rlk, level, ep, nb, w, s);
         if (r) return r;
     }
@@ -852,7 +982,7 @@ int op_rotate(helr_ctx* c, const u64* a, long long as, long long galois, const u
         KsWs w = ks_ws(c, chunk);
         const u64* ab = a + (size_t)b0 * as;
         KsInput in{ab + (size_t)c->L * c->n, as, g};
-        KsEpilogue ep{out + (size_t)b0 * os, os, accumulate ? ab : nullptr, as, ab, as, g};
+        KsEpilogue ep = make_epilogue(out + (size_t)b0 * os, os, accumulate ? ab : nullptr, as, ab, as, 1, &g);
         int r = keyswitch_batch(c, in, gk, level, ep, nb, w, s);
         if (r) return r;
     }

@@ -18,3 +18,7 @@ int op_rotate(helr_ctx* c, const u64* a, long long as, long long galois, const u
               int count, int level, int accumulate, cudaStream_t s);
 int op_lincomb(helr_ctx* c, int terms, const u64* const* x, const long long* xs, const u64* const* k, u64* out,
                long long os, int count, int level, cudaStream_t s);
+// out = [a +] sum_{t < nsteps} rot_{gal[t]}(a): one ModUp, summed inner
+// products in the extended basis, one ModDown (double hoisting)
+int op_rotsum_hoisted(helr_ctx* c, const u64* a, long long as, int nsteps, const long long* gal, const u64* const* keys,
+                      u64* out, long long os, int count, int level, int include_identity, cudaStream_t s);

@@ -50,7 +50,7 @@ class NagArgs(ctypes.Structure):
         ("rot_left", ctypes.POINTER(ctypes.c_void_p)), ("rot_right", ctypes.POINTER(ctypes.c_void_p)),
         ("rot_rows", ctypes.POINTER(ctypes.c_void_p)),
         ("mask_pt", ctypes.c_void_p), ("consts", ctypes.c_void_p), ("grad", ctypes.c_void_p),
-        ("phase", ctypes.c_int),
+        ("phase", ctypes.c_int), ("log_baby", ctypes.c_int),
     ]
 
 
@@ -84,14 +84,22 @@ def _rint(x: float) -> int:
     return int(np.rint(x))
 
 
+OUT_SCALE_BITS = 50  # scale of W', V' at the bottom level: |W| < q_0 / 2^51 = 2^9
+
+
 def plan_iteration(ck, lw: int, s_w: float, s_v: float, s_z: float, s_b: float, qpoly, mult: float,
-                   eta: float) -> IterPlan:
+                   eta: float, out_bits: int = OUT_SCALE_BITS) -> IterPlan:
     """Constants of one depth-7 iteration starting with W, V at level ``lw``.
 
     qpoly = (q0, q1, q2, q3): coefficients of 1 - sigmoid_poly (the
     complement, enctrain.py:155-159, sigmoid.py:72-76); mult = 1 + gamma
     (enhanced) or gamma (baseline), eta = (1 - alpha0) / alpha1
     (enctrain.py:362-366, 224-229).
+
+    Precision: every integer constant is kept >= 2^30 (relative rounding
+    <= 2^-30): the NAG constants scale with s_out / s_d, so W', V' land on
+    2^out_bits rather than the canonical bottom-level scale, and B̄ arrives
+    pre-scaled (s_b = 2^40 / max|B̄|) so its encryption noise is negligible.
     """
     if lw < ITER_DEPTH or lw >= ck.L:
         raise ValueError(f"iteration needs W at a level in [{ITER_DEPTH}, {ck.L}), got {lw}")
@@ -111,7 +119,7 @@ def plan_iteration(ck, lw: int, s_w: float, s_v: float, s_z: float, s_b: float, 
     c2 = _rint(q2 * s_c * q[l - 3] / s_u2)
     c0 = _rint(q0 * s_c)
     s_d = s_s * s_b / q[l - 5]
-    s_out = D[l - 7]
+    s_out = float(2 ** out_bits) if l - 7 == 0 else D[l - 7]
     f = s_out * q[l - 6]
     cw1 = _rint(f / s_w)
     ca1 = _rint(mult * f / s_d)
@@ -151,7 +159,7 @@ class FusedTrainer:
 
     def __init__(self, ctx: GpuContext, ds, rows_per_block: int, blocks_per_batch: int = 1,
                  mode: str = "mini_batch", poly: PolyApprox = BASELINE_CUBIC, schedule=None,
-                 epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False):
+                 epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False, bsgs: bool = True):
         if mode not in ("mini_batch", "full_batch"):
             raise ValueError(f"mode must be mini_batch or full_batch, got {mode!r}")
         from .optimizer import ExpDecay
@@ -172,6 +180,8 @@ class FusedTrainer:
         self.log_g = int(math.log2(lay.g))
         self.log_m = int(math.log2(lay.m))
         self.batch_rows = lay.m * blocks_per_batch
+        # sum_col_vec halves by baby-step/giant-step hoisted groups (log_baby > 0)
+        self.log_baby = (self.log_g + 1) // 2 if (bsgs and self.log_g > 0) else 0
         self.qpoly = poly.complement().padded(3)
         self.lib = _lib.load()
         _bind(self.lib)
@@ -219,10 +229,13 @@ class FusedTrainer:
         self.bbar = torch.empty((bb.shape[0], C, 2, L, N), dtype=torch.int64, device=ctx.device)
         bflat = bb.reshape(-1, ck.slots)
         bout = self.bbar.view(-1, 2, L, N)
+        # B̄ entries are small (1e-3 per 1,024-row batch, ~1e-5 merged over the
+        # whole dataset); encode them at s_top / max|B̄| so the encryption noise
+        # stays ~2^-30 relative to B̄ (the planner tracks the exact scale)
+        self.s_b = s_top / float(np.max(np.abs(bb)))
         for s in range(0, bflat.shape[0], chunk):
-            coef = ctx.encoder.encode(bflat[s:s + chunk], s_top)
+            coef = ctx.encoder.encode(bflat[s:s + chunk], self.s_b)
             ctx.encrypt_to(coef, bout[s:s + coef.shape[0]], top)
-        self.s_b = s_top
         # W0 = V0 = enc(0) at the top level (enctrain.py:145-151)
         self.wv = torch.empty((2 * C, 2, L, N), dtype=torch.int64, device=ctx.device)
         ctx.encrypt_to(np.zeros((2 * C, N), dtype=np.int64), self.wv, top)
@@ -234,14 +247,23 @@ class FusedTrainer:
         self.t = 0
         # keys: left/right 2^i (sum_col_vec), g*2^i (sum_rows)
         S = ck.slots
-        self.gal_left = [pow(5, 1 << i, 2 * N) for i in range(self.log_g)]
-        self.gal_right = [pow(5, S - (1 << i), 2 * N) for i in range(self.log_g)]
+        if self.log_baby > 0:
+            bs, gs = self.log_baby, self.log_g - self.log_baby
+            steps = list(range(1, 1 << bs)) + [k << bs for k in range(1, 1 << gs)]
+        else:
+            steps = [1 << i for i in range(self.log_g)]
+        self.gal_left = [pow(5, k, 2 * N) for k in steps]
+        self.gal_right = [pow(5, S - k, 2 * N) for k in steps]
         self.gal_rows = [pow(5, lay.g << i, 2 * N) for i in range(self.log_m)]
         keys = lambda gs: (ctypes.c_void_p * max(1, len(gs)))(*[ctx.galois_key(g).data_ptr() for g in gs])
         self._k_left, self._k_right, self._k_rows = keys(self.gal_left), keys(self.gal_right), keys(self.gal_rows)
         self._masks: dict = {}
         self.consts_dev = torch.zeros((NCONST, L), dtype=torch.int64, device=ctx.device)
-        self.consts_host = torch.zeros((NCONST, L), dtype=torch.int64).pin_memory()
+        # ring of pinned host buffers: an async H2D copy must never read a host
+        # buffer that a later iteration has already overwritten
+        self._cring = [torch.zeros((NCONST, L), dtype=torch.int64).pin_memory() for _ in range(4)]
+        self._cev = [None] * len(self._cring)
+        self._ci = 0
         self.grad = torch.empty((C, 2, L, N), dtype=torch.int64, device=ctx.device)
         self.zstage = torch.empty((R, C, 2, L, N), dtype=torch.int64, device=ctx.device)
         self.bstage = torch.empty((C, 2, L, N), dtype=torch.int64, device=ctx.device)
@@ -318,11 +340,20 @@ class FusedTrainer:
                        w=self.wv.data_ptr(), v=self.wv.data_ptr() + C * cs, bbar=self.bstage.data_ptr(),
                        lw=plan.lw, rlk=self.ctx.rlk.data_ptr(), rot_left=self._k_left, rot_right=self._k_right,
                        rot_rows=self._k_rows, mask_pt=self._mask(plan.lw, plan.mask_scale).data_ptr(),
-                       consts=self.consts_dev.data_ptr(), grad=self.grad.data_ptr(), phase=phase)
+                       consts=self.consts_dev.data_ptr(), grad=self.grad.data_ptr(), phase=phase,
+                       log_baby=self.log_baby)
 
     def _upload_consts(self, plan: IterPlan):
-        self.consts_host.copy_(torch.from_numpy(plan.consts.view(np.int64)))
-        self.consts_dev.copy_(self.consts_host, non_blocking=True)
+        i = self._ci
+        self._ci = (i + 1) % len(self._cring)
+        if self._cev[i] is not None:
+            self._cev[i].synchronize()
+        buf = self._cring[i]
+        buf.copy_(torch.from_numpy(plan.consts.view(np.int64)))
+        self.consts_dev.copy_(buf, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._cev[i] = ev
 
     def _stage(self, batch: int, bbar_index: int, with_bbar: bool = True):
         src_z = self.z_host if self.host_stream else self.z

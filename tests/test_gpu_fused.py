@@ -32,7 +32,7 @@ CASES = {
 }
 
 
-def _setup(case, seed=11):
+def _setup(case, seed=11, bsgs=False):
     log_n, L, dnum, R, C, log_g = CASES[case]
     P = CkksParams.generate(log_n=log_n, n_q=L, dnum=dnum)
     ctx = GpuContext(P, seed=seed, max_batch=4)
@@ -52,8 +52,13 @@ def _setup(case, seed=11):
     ctx.encrypt_to(ctx.encoder.encode(bvals, s_top), bbar, top)
     qpoly = BASELINE_CUBIC.complement().padded(3)
     plan = plan_iteration(P, top, s_top, s_top, s_top, s_top, qpoly, 1.05, 0.37)
-    gl = [pow(5, 1 << i, 2 * n) for i in range(log_g)]
-    gr = [pow(5, S - (1 << i), 2 * n) for i in range(log_g)]
+    log_baby = (log_g + 1) // 2 if bsgs else 0
+    if log_baby:
+        steps = list(range(1, 1 << log_baby)) + [k << log_baby for k in range(1, 1 << (log_g - log_baby))]
+    else:
+        steps = [1 << i for i in range(log_g)]
+    gl = [pow(5, k, 2 * n) for k in steps]
+    gr = [pow(5, S - k, 2 * n) for k in steps]
     gw = [pow(5, (1 << log_g) << i, 2 * n) for i in range(log_m)]
     arr = lambda gs: (ctypes.c_void_p * max(1, len(gs)))(*[ctx.galois_key(g).data_ptr() for g in gs])
     mask = ctx._plain(ctx.encoder.encode(row_mask(S, 1 << log_g), plan.mask_scale), top - 1)
@@ -61,7 +66,7 @@ def _setup(case, seed=11):
     grad = ctx._empty((C, 2, L, n))
     keys = (arr(gl), arr(gr), arr(gw))
     return dict(P=P, ctx=ctx, z=z, wv=wv, bbar=bbar, plan=plan, mask=mask, consts=consts, grad=grad, keys=keys,
-                R=R, C=C, log_g=log_g, log_m=log_m, gals=gl + gr + gw, vals=(zvals, wv_vals, bvals))
+                R=R, C=C, log_g=log_g, log_m=log_m, gals=gl + gr + gw, vals=(zvals, wv_vals, bvals), log_baby=log_baby)
 
 
 def _args(d, z_ptr, phase):
@@ -71,7 +76,7 @@ def _args(d, z_ptr, phase):
                    v=d["wv"].data_ptr() + C * cs, bbar=d["bbar"].data_ptr(), lw=d["P"].top_level,
                    rlk=ctx.rlk.data_ptr(), rot_left=d["keys"][0], rot_right=d["keys"][1], rot_rows=d["keys"][2],
                    mask_pt=d["mask"].data_ptr(), consts=d["consts"].data_ptr(), grad=d["grad"].data_ptr(),
-                   phase=phase)
+                   phase=phase, log_baby=d["log_baby"])
 
 
 def _oracle_inputs(d):
@@ -81,9 +86,10 @@ def _oracle_inputs(d):
     return orc, gkeys, u64(ctx.rlk), u64(d["mask"]), d["plan"].consts
 
 
+@pytest.mark.parametrize("bsgs", [False, True])
 @pytest.mark.parametrize("case", list(CASES))
-def test_fused_iteration_matches_oracle(case):
-    d = _setup(case)
+def test_fused_iteration_matches_oracle(case, bsgs):
+    d = _setup(case, bsgs=bsgs)
     ctx, C = d["ctx"], d["C"]
     lib = _lib.load()
     _bind(lib)
@@ -93,7 +99,8 @@ def test_fused_iteration_matches_oracle(case):
                "nag")
     orc, gkeys, rlk, mask, consts = _oracle_inputs(d)
     lw = d["P"].top_level
-    w2, v2 = osched.nag_iteration(orc, z_np, w_np, v_np, b_np, lw, rlk, gkeys, mask, consts, d["log_g"], d["log_m"])
+    w2, v2 = osched.nag_iteration(orc, z_np, w_np, v_np, b_np, lw, rlk, gkeys, mask, consts, d["log_g"], d["log_m"],
+                                  log_baby=d["log_baby"])
     out = u64(d["wv"])
     lo = lw - 7 + 1
     np.testing.assert_array_equal(out[:C, :, :lo], w2[:, :, :lo])
@@ -130,9 +137,10 @@ def test_fused_full_batch_phases_match_oracle():
     np.testing.assert_array_equal(out[C:, :, :lo], v2[:, :, :lo])
 
 
-def test_fused_iteration_values():
+@pytest.mark.parametrize("bsgs", [False, True])
+def test_fused_iteration_values(bsgs):
     """Decrypted W', V' equal the plaintext update within CKKS noise."""
-    d = _setup("toy_shape", seed=5)
+    d = _setup("toy_shape", seed=5, bsgs=bsgs)
     ctx, C, R = d["ctx"], d["C"], d["R"]
     P = d["P"]
     lib = _lib.load()
@@ -178,5 +186,6 @@ def test_fused_iteration_values():
               torch.cuda.current_stream().cuda_stream)
     coef = out.cpu().numpy()
     got = ctx.encoder.decode(coef, d["plan"].s_out)
-    np.testing.assert_allclose(got[:C].real, Wn, atol=1e-5)
-    np.testing.assert_allclose(got[C:].real, Vn, atol=1e-5)
+    err = max(np.abs(got[:C].real - Wn).max(), np.abs(got[C:].real - Vn).max())
+    print(f"fused step value error (bsgs={bsgs}): {err:.3e}")
+    assert err < 1e-6

@@ -176,3 +176,24 @@ def test_refresh(pair, rng):
                   2, ctx.enc_seed, 777, stream())
         exp = orc.refresh(sk, ref, 1, ratio, P.top_level, ctx.enc_seed, 777)
         np.testing.assert_array_equal(u64(out), exp)
+
+
+@pytest.mark.parametrize("steps,ident", [((1, 2, 3), 1), ((4, 8, 12), 0), ((-1, -5), 1)])
+def test_rotsum_hoisted(pair, rng, steps, ident):
+    import ctypes
+    P, ctx, orc, sk = pair
+    z, cts, ref = _fresh(ctx, orc, sk, rng, count=2)
+    gals = [ctx.galois_for_rotation(k) for k in steps]
+    keys = [ctx.galois_key(g) for g in gals]
+    lvl = P.top_level - 1
+    a = torch.stack([c.data for c in cts])
+    out = ctx._empty((2, 2, P.L, P.n))
+    garr = (ctypes.c_int64 * len(gals))(*gals)
+    karr = (ctypes.c_void_p * len(keys))(*[k.data_ptr() for k in keys])
+    _lib.call("helr_rotsum", ctx.handle, a.data_ptr(), len(gals), garr, karr, out.data_ptr(), 2, lvl, ident, stream())
+    exp = orc.rotsum(ref, gals, [u64(k) for k in keys], lvl, include_identity=bool(ident))
+    np.testing.assert_array_equal(u64(out)[:, :, : lvl + 1], exp[:, :, : lvl + 1])
+    # values: decrypt == sum of np.roll (hesim.py:222 semantics)
+    want = sum(np.roll(z[0], -k) for k in steps) + (z[0] if ident else 0)
+    dec = ctx.encoder.decode(orc.decrypt(sk, exp[:1], lvl)[0], cts[0].scale)
+    assert np.abs(dec - want).max() < 1e-6
