@@ -72,6 +72,10 @@ int helr_ntt_inv(helr_ctx* ctx, uint64_t* data, int first_prime, int n_limbs,
 /* ---- keys (client side; not in the reference, which has no keys) ------- */
 
 int helr_keygen_secret(helr_ctx* ctx, uint64_t* sk, uint64_t seed, void* stream);
+/* Sparse ternary secret with exactly hw nonzero +-1 coefficients (hw = 0:
+ * uniform ternary, as helr_keygen_secret).  Lower secret weight shrinks the
+ * rescale / key-switching rounding noise by ~sqrt(hw / (2N/3)). */
+int helr_keygen_secret_hw(helr_ctx* ctx, uint64_t* sk, uint64_t seed, int hw, void* stream);
 /* galois == 0: relinearisation key (s^2 -> s); otherwise key for X -> X^galois. */
 int helr_keygen_switch(helr_ctx* ctx, const uint64_t* sk, int64_t galois,
                        uint64_t* evk, uint64_t seed, uint64_t key_id, void* stream);

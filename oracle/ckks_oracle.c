@@ -200,11 +200,38 @@ static void automorph_poly(oc_ctx* c, const u64* in, u64* out, u64 g) {
 }
 
 /* ---------------- keys ---------------- */
-void oc_keygen_secret(oc_ctx* c, u64 seed, u64* sk) {
+/* Secret coefficients.  hw == 0: uniform ternary.  hw > 0: exactly hw
+ * nonzero +-1 entries (HEAAN's sparse secret): the hw positions with the
+ * smallest prng(seed, SK/0, i) (ties broken by index), sign from bit 0 of
+ * prng(seed, SK/1, i).  Host-side client key generation, same rule on device. */
+typedef struct { u64 r; int i; } rank_t;
+static int rank_cmp(const void* a, const void* b) {
+    const rank_t *x = (const rank_t*)a, *y = (const rank_t*)b;
+    if (x->r != y->r) return x->r < y->r ? -1 : 1;
+    return x->i - y->i;
+}
+void oc_secret_coeffs(u64 seed, int N, int hw, int64_t* s) {
+    u64 st = stream_id(ST_SK, 0, 0, PU_S);
+    if (hw <= 0) {
+        for (int i = 0; i < N; i++) s[i] = (int64_t)(oc_prng(seed, st, (u64)i) % 3) - 1;
+        return;
+    }
+    rank_t* rk = (rank_t*)malloc(sizeof(rank_t) * N);
+    for (int i = 0; i < N; i++) { rk[i].r = oc_prng(seed, st, (u64)i); rk[i].i = i; }
+    qsort(rk, N, sizeof(rank_t), rank_cmp);
+    u64 sg = stream_id(ST_SK, 0, 1, PU_S);
+    for (int i = 0; i < N; i++) s[i] = 0;
+    for (int k = 0; k < hw && k < N; k++) {
+        int i = rk[k].i;
+        s[i] = (oc_prng(seed, sg, (u64)i) & 1) ? 1 : -1;
+    }
+    free(rk);
+}
+
+void oc_keygen_secret_hw(oc_ctx* c, u64 seed, int hw, u64* sk) {
     int N = c->n;
     int64_t* s = (int64_t*)malloc(sizeof(int64_t) * N);
-    u64 st = stream_id(ST_SK, 0, 0, PU_S);
-    for (int i = 0; i < N; i++) s[i] = (int64_t)(oc_prng(seed, st, (u64)i) % 3) - 1;
+    oc_secret_coeffs(seed, N, hw, s);
 #pragma omp parallel for
     for (int p = 0; p < c->L + c->K; p++) {
         u64* d = sk + (size_t)p * N;
@@ -213,6 +240,7 @@ void oc_keygen_secret(oc_ctx* c, u64 seed, u64* sk) {
     }
     free(s);
 }
+void oc_keygen_secret(oc_ctx* c, u64 seed, u64* sk) { oc_keygen_secret_hw(c, seed, 0, sk); }
 
 /* P mod q_i for i < L */
 static u64 pmod(oc_ctx* c, int i) {

@@ -52,6 +52,8 @@ def lib():
             "oc_intt": (None, [vp, _u64p, ctypes.c_int]),
             "oc_ntt_batch": (None, [vp, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int]),
             "oc_keygen_secret": (None, [vp, ctypes.c_uint64, _u64p]),
+            "oc_keygen_secret_hw": (None, [vp, ctypes.c_uint64, ctypes.c_int, _u64p]),
+            "oc_secret_coeffs": (None, [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, _i64p]),
             "oc_keygen_switch": (None, [vp, _u64p, ctypes.c_int64, _u64p, ctypes.c_uint64, ctypes.c_uint64]),
             "oc_encrypt": (None, [vp, _u64p, _i64p, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64]),
             "oc_decrypt": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_int, _i64p]),
@@ -141,10 +143,17 @@ class Oracle:
         return out
 
     # keys
-    def keygen_secret(self, seed: int) -> np.ndarray:
+    def keygen_secret(self, seed: int, hw: int = 0) -> np.ndarray:
+        """NTT-form secret over every prime; hw = 0 uniform ternary, else
+        exactly hw nonzero +-1 coefficients."""
         sk = np.zeros((self.L + self.K, self.N), dtype=np.uint64)
-        lib().oc_keygen_secret(self._h, seed, _p(sk))
+        lib().oc_keygen_secret_hw(self._h, seed, hw, _p(sk))
         return sk
+
+    def secret_coeffs(self, seed: int, hw: int = 0) -> np.ndarray:
+        s = np.zeros(self.N, dtype=np.int64)
+        lib().oc_secret_coeffs(seed, self.N, hw, _p(s))
+        return s
 
     def keygen_switch(self, sk, galois: int, seed: int, key_id: int) -> np.ndarray:
         evk = self.key_zeros()

@@ -37,6 +37,7 @@ SIGNATURES = {
     "helr_ntt_fwd": [_vp, _u64p, _i, _i, _i, _i64, _vp],
     "helr_ntt_inv": [_vp, _u64p, _i, _i, _i, _i64, _vp],
     "helr_keygen_secret": [_vp, _u64p, _u64, _vp],
+    "helr_keygen_secret_hw": [_vp, _u64p, _u64, _i, _vp],
     "helr_keygen_switch": [_vp, _u64p, _i64, _u64p, _u64, _u64, _vp],
     "helr_encrypt": [_vp, _u64p, _u64p, _u64p, _i, _i, _u64, _u64, _vp],
     "helr_decrypt": [_vp, _u64p, _u64p, _i, _i, _u64p, _vp],

@@ -119,7 +119,7 @@ class GpuContext:
         self._h = handle
         self._residue_cache: dict = {}
         self.sk = self._empty((ckks.L + ckks.K, ckks.n))
-        self._call("helr_keygen_secret", _ptr(self.sk), self.key_seed, _stream())
+        self._call("helr_keygen_secret_hw", _ptr(self.sk), self.key_seed, ckks.hw, _stream())
         self.rlk = self._switch_key(0)
         self._gks: dict[int, torch.Tensor] = {}
 

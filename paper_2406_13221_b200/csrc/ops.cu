@@ -12,7 +12,10 @@
 // (ModUp), NTT, inner product with the key, ModDown by P.  All `count`
 // ciphertexts of a call go through every stage together so each key limb is
 // read once per call (key batching across the row blocks of a mini-batch).
+#include <algorithm>
 #include <cstdio>
+#include <utility>
+#include <vector>
 
 #include "../../include/helr_ckks.h"
 #include "ntt.cuh"
@@ -163,6 +166,13 @@ __global__ void k_fill_secret(u64* sk, int n, int LK, u64 seed, Tables tb) {
     }
 }
 
+__global__ void k_secret_from_coeffs(u64* sk, const signed char* s8, int n, int LK, Tables tb) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const long long sv = s8[i];
+        for (int p = 0; p < LK; p++) sk[(size_t)p * n + i] = reduce_i64(sv, tb.q[p]);
+    }
+}
+
 extern "C" int helr_keygen_secret(helr_ctx* c, uint64_t* sk, uint64_t seed, void* s) {
     clear_stale_error("helr_keygen_secret");
     k_fill_secret<<<blocks_for(c->n, 256), 256, 0, S(s)>>>((u64*)sk, c->n, c->LK, seed, c->t);
@@ -170,6 +180,37 @@ extern "C" int helr_keygen_secret(helr_ctx* c, uint64_t* sk, uint64_t seed, void
     LimbMap m = limb_range(0, c->LK);
     ntt_buffers<false>(c, (const u64*)sk, 0, (u64*)sk, 0, m, 1, S(s));
     CHECK_LAUNCH("keygen_secret ntt");
+    return HELR_OK;
+}
+
+// Sparse ternary secret with exactly hw nonzero +-1 coefficients (HEAAN's
+// default family): positions = the hw smallest prng(seed, SK/0, i), ties by
+// index; sign = bit 0 of prng(seed, SK/1, i).  Selected on the host (client
+// key generation), identical rule in oracle/ckks_oracle.c oc_secret_coeffs.
+extern "C" int helr_keygen_secret_hw(helr_ctx* c, uint64_t* sk, uint64_t seed, int hw, void* s) {
+    clear_stale_error("helr_keygen_secret_hw");
+    if (hw <= 0) return helr_keygen_secret(c, sk, seed, s);
+    const int n = c->n;
+    const u64 key = prng_key(seed, stream_id(ST_SK, 0, 0, PU_S));
+    const u64 ksg = prng_key(seed, stream_id(ST_SK, 0, 1, PU_S));
+    std::vector<std::pair<u64, int>> rk(n);
+    for (int i = 0; i < n; i++) rk[i] = {prng_at(key, (u64)i), i};
+    std::sort(rk.begin(), rk.end());
+    std::vector<signed char> s8(n, 0);
+    for (int k = 0; k < hw && k < n; k++) {
+        const int i = rk[k].second;
+        s8[i] = (prng_at(ksg, (u64)i) & 1) ? 1 : -1;
+    }
+    signed char* d8 = nullptr;
+    if (!cuda_ok(cudaMalloc(&d8, n), "cudaMalloc(secret)")) return HELR_ECUDA;
+    if (!cuda_ok(cudaMemcpy(d8, s8.data(), n, cudaMemcpyHostToDevice), "upload secret")) { cudaFree(d8); return HELR_ECUDA; }
+    k_secret_from_coeffs<<<blocks_for(n, 256), 256, 0, S(s)>>>((u64*)sk, d8, n, c->LK, c->t);
+    CHECK_KERNEL("keygen_secret_hw");
+    LimbMap m = limb_range(0, c->LK);
+    ntt_buffers<false>(c, (const u64*)sk, 0, (u64*)sk, 0, m, 1, S(s));
+    CHECK_LAUNCH("keygen_secret_hw ntt");
+    cudaStreamSynchronize(S(s));
+    cudaFree(d8);
     return HELR_OK;
 }
 
@@ -821,6 +862,10 @@ __device__ __forceinline__ u64 reduce192(const u192v& a, u64 q, u64 r1, u64 r0, 
     if (a.hi) r = add_mod(r, shoup(a.hi, t128, t128_sh, q), q);
     return r;
 }
+// All loads of one rotation step are issued before its multiply-accumulates
+// (nd <= MAXD digits held in registers) so each thread keeps ~3*nd loads in
+// flight; two steps are unrolled for more memory-level parallelism.
+template <int MAXD>
 __global__ void k_ks_inner_hoisted(const u64* ext, long long ext_item_stride, long long ext_digit_stride, HoistKeys hk,
                                    u64* acc, long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK,
                                    int nd, int B, Tables tb, const u64* one_sh, const u64* t128, const u64* t128_sh) {
@@ -832,13 +877,28 @@ __global__ void k_ks_inner_hoisted(const u64* ext, long long ext_item_stride, lo
     const u64 q = tb.q[p];
     u192v a0{0, 0, 0}, a1{0, 0, 0};
     const u64* xb = ext + (size_t)b * ext_item_stride + (size_t)e * n;
+    const size_t k0off = ((size_t)p) * n + i;             // + j*2*LK*n
+    const size_t k1off = ((size_t)LK + p) * n + i;
+    const size_t kds = (size_t)2 * LK * n;
+#pragma unroll 2
     for (int t = 0; t < hk.nsteps; t++) {
         const int src = galois_perm(i, (u64)hk.gal[t], log_n);
         const u64* kt = hk.key[t];
-        for (int j = 0; j < nd; j++) {
-            const u64 u = xb[(size_t)j * ext_digit_stride + src];
-            mac192(a0, u, kt[(((size_t)j * 2) * LK + p) * n + i]);
-            mac192(a1, u, kt[(((size_t)j * 2 + 1) * LK + p) * n + i]);
+        u64 u[MAXD], k0[MAXD], k1[MAXD];
+#pragma unroll
+        for (int j = 0; j < MAXD; j++) {
+            if (j < nd) {
+                u[j] = xb[(size_t)j * ext_digit_stride + src];
+                k0[j] = __ldg(kt + (size_t)j * kds + k0off);
+                k1[j] = __ldg(kt + (size_t)j * kds + k1off);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < MAXD; j++) {
+            if (j < nd) {
+                mac192(a0, u[j], k0[j]);
+                mac192(a1, u[j], k1[j]);
+            }
         }
     }
     u64* ap = acc + (size_t)b * acc_item_stride;
@@ -881,8 +941,9 @@ int op_rotsum_hoisted(helr_ctx* c, const u64* a, long long as, int nsteps, const
             const int by = nb < 4 ? nb : 4;
             dim3 g(blocks_for(n, 64), (nb + by - 1) / by, ne);
             ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne * nsteps + 2.0 * nd * ne * nsteps + 2.0 * nb * ne), s);
-            k_ks_inner_hoisted<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, hk, w.acc, w.acc_s, n, c->log_n, nl,
-                                                          K, L, c->LK, nd, nb, c->t, c->one_sh, c->t128, c->t128_sh);
+            auto kern = nd <= 4 ? k_ks_inner_hoisted<4> : (nd <= 8 ? k_ks_inner_hoisted<8> : k_ks_inner_hoisted<32>);
+            kern<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, hk, w.acc, w.acc_s, n, c->log_n, nl, K, L, c->LK,
+                                            nd, nb, c->t, c->one_sh, c->t128, c->t128_sh);
             CHECK_KERNEL("rotsum inner");
         }
         KsEpilogue ep = make_epilogue(out + (size_t)b0 * os, os, include_identity ? ab : nullptr, as, ab, as, nsteps, gg);

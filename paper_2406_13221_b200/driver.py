@@ -159,7 +159,8 @@ class FusedTrainer:
 
     def __init__(self, ctx: GpuContext, ds, rows_per_block: int, blocks_per_batch: int = 1,
                  mode: str = "mini_batch", poly: PolyApprox = BASELINE_CUBIC, schedule=None,
-                 epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False, bsgs: bool = True):
+                 epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False, bsgs: bool = True,
+                 refresh_bits: int = 45):
         if mode not in ("mini_batch", "full_batch"):
             raise ValueError(f"mode must be mini_batch or full_batch, got {mode!r}")
         from .optimizer import ExpDecay
@@ -172,6 +173,10 @@ class FusedTrainer:
         self.epsilon = epsilon
         self.enhanced = enhanced
         self.use_graph = use_graph
+        # W, V re-enter each iteration at scale 2^refresh_bits: above Delta = 2^40
+        # so the refresh's fresh encryption noise is negligible, below 2^50 so
+        # the row-start mask still encodes at >= 2^35
+        self.refresh_bits = refresh_bits
         self.layout: BlockLayout = plan_layout(ds.n_samples, ds.n_features, ctx.params, rows_per_block)
         lay = self.layout
         self.rows = blocks_per_batch
@@ -324,14 +329,15 @@ class FusedTrainer:
         """Refresh stand-in on W and V (NOT bootstrapping; see helr_refresh)."""
         ck = self.ck
         top = ck.top_level
-        ratio = ck.level_scales[top] / self.s_w
+        target = float(2 ** self.refresh_bits)
+        ratio = target / self.s_w
         first = self.ctx._take_ct_ids(self.wv.shape[0])
         stream = torch.cuda.current_stream().cuda_stream
         self.ctx._call("helr_refresh", self.ctx.sk.data_ptr(), self.wv.data_ptr(), self.level, float(ratio),
                        self.wv_tmp.data_ptr(), top, self.wv.shape[0], self.ctx.enc_seed, first, stream)
         self.wv.copy_(self.wv_tmp)
         self.level = top
-        self.s_w = self.s_v = ck.level_scales[top]
+        self.s_w = self.s_v = target
 
     def _args(self, plan: IterPlan, phase: int) -> NagArgs:
         C = self.cols

@@ -190,6 +190,7 @@ class CkksParams:
     dnum: int
     scale_bits: int = 40
     cbd_eta: int = 21
+    secret_hw: int = 64
     psi: tuple = field(default=(), compare=False)
 
     def __post_init__(self):
@@ -217,13 +218,13 @@ class CkksParams:
 
     @classmethod
     def generate(cls, log_n: int, n_q: int, dnum: int = 3, scale_bits: int = 40,
-                 q0_bits: int = 60, p_bits: int = 61, cbd_eta: int = 21) -> "CkksParams":
+                 q0_bits: int = 60, p_bits: int = 61, cbd_eta: int = 21, secret_hw: int = 64) -> "CkksParams":
         alpha = -(-n_q // dnum)
         q0 = ntt_primes(log_n, q0_bits, 1, mode="below")
         scaling = ntt_primes(log_n, scale_bits, n_q - 1, mode="closest", exclude=tuple(q0))
         special = ntt_primes(log_n, p_bits, alpha, mode="below", exclude=tuple(q0 + scaling))
         return cls(log_n=log_n, q=tuple(q0 + scaling), p=tuple(special), dnum=dnum,
-                   scale_bits=scale_bits, cbd_eta=cbd_eta)
+                   scale_bits=scale_bits, cbd_eta=cbd_eta, secret_hw=secret_hw)
 
     # -- derived -------------------------------------------------------------
 
@@ -234,6 +235,12 @@ class CkksParams:
     @property
     def slots(self) -> int:
         return 1 << (self.log_n - 1)
+
+    @property
+    def hw(self) -> int:
+        """Effective secret Hamming weight (0 = uniform ternary); capped at N/2
+        for tiny test rings."""
+        return min(self.secret_hw, self.n // 2) if self.secret_hw > 0 else 0
 
     @property
     def L(self) -> int:

@@ -44,7 +44,7 @@ def pair(request):
     P = RINGS[request.param]
     ctx = GpuContext(P, seed=5, max_batch=4)
     orc = Oracle(P)
-    sk = orc.keygen_secret(ctx.key_seed)
+    sk = orc.keygen_secret(ctx.key_seed, P.hw)
     return P, ctx, orc, sk
 
 

@@ -25,12 +25,13 @@ CFG = {
 }
 
 
-def run(name):
+def run(name, refresh_bits=45):
     make, log_n, rows, blocks, mode = CFG[name]
     gold = np.load(ROOT / "tests" / "golden" / f"{name}.npz")
     ds = make()
     ctx = GpuContext(CkksParams.generate(log_n=log_n, n_q=8, dnum=3), seed=2, max_batch=8)
-    tr = FusedTrainer(ctx, ds, rows_per_block=rows, blocks_per_batch=blocks, mode=mode, use_graph=True)
+    tr = FusedTrainer(ctx, ds, rows_per_block=rows, blocks_per_batch=blocks, mode=mode, use_graph=True,
+                      refresh_bits=refresh_bits)
     its = [int(x) for x in gold["iterations"]]
     worst_w = worst_a = 0.0
     curve = []
@@ -44,7 +45,7 @@ def run(name):
             da = abs(auroc(ds.y, ds.X @ w) - float(gold["auc"][k]))
             worst_w, worst_a = max(worst_w, dw), max(worst_a, da)
             curve.append((t, dw, da))
-    out = dict(workload=name, iterations=its[-1], max_abs_dw=worst_w, max_abs_dauc=worst_a,
+    out = dict(workload=name, refresh_bits=refresh_bits, iterations=its[-1], max_abs_dw=worst_w, max_abs_dauc=worst_a,
                final_auc=float(gold["auc"][-1]), seconds=time.time() - t0,
                curve=curve if len(curve) < 400 else [c for c in curve if c[0] % 16 == 0])
     print(json.dumps(out), flush=True)
@@ -52,5 +53,6 @@ def run(name):
 
 
 if __name__ == "__main__":
-    for name in sys.argv[1:] or ["toy", "medium", "paper_mini"]:
-        run(name)
+    for spec in sys.argv[1:] or ["toy", "medium", "paper_mini"]:
+        name, _, bits = spec.partition(":")
+        run(name, int(bits) if bits else 45)
