@@ -121,6 +121,12 @@ int helr_rescale(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count,
 int helr_mul_relin(helr_ctx* ctx, const uint64_t* a, const uint64_t* b,
                    const uint64_t* rlk, uint64_t* out, int count, int level,
                    void* stream);
+/* ct x ct product, relinearised and rescaled in one key switch: the
+ * accumulator gets P*(d0, d1) and a single centred ModDown divides by
+ * P*q_level (SimContext.mul, hesim.py:186-195).  Output at level-1. */
+int helr_mul_relin_rescale(helr_ctx* ctx, const uint64_t* a, const uint64_t* b,
+                           const uint64_t* rlk, uint64_t* out, int count, int level,
+                           void* stream);
 /* Multiply by X^(N/2) (slots * i). */
 int helr_imul(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count,
               int level, void* stream);

@@ -615,6 +615,91 @@ void oc_keyswitch(oc_ctx* c, const u64* d, const u64* evk, int level, u64* k0, u
     free(up); free(acc);
 }
 
+/* ct x ct product, relinearised and rescaled by ONE centred division by
+ * M = P * q_l (device helr_mul_relin_rescale): acc = sum_j ModUp(d2)_j evk_j,
+ * acc_Q += P * (d0, d1), then out_i = (acc_i - conv_i) * M^-1 for i < l where
+ * conv is the centred conversion of acc mod M from {p_0..p_{K-1}, q_l}. */
+void oc_tensor(oc_ctx* c, const u64* a, const u64* b, u64* d, int level);
+/* from a tensor d = [d0, d1, d2] (u64[3][L][N]) to one ciphertext at level-1 */
+void oc_relin_rescale_tensor(oc_ctx* c, const u64* d, const u64* rlk, u64* out, int level) {
+    int N = c->n, L = c->L, K = c->K, al = c->alpha;
+    int nl = level + 1, ext = nl + K, nd = (nl + al - 1) / al, l = level, ns = K + 1;
+    const int x = 0;
+    {
+        u64* up = (u64*)malloc(sizeof(u64) * (size_t)nd * ext * N);
+        u64* acc = (u64*)calloc((size_t)2 * ext * N, sizeof(u64));
+        u64* src = (u64*)malloc(sizeof(u64) * (size_t)ns * N);
+        u64* conv = (u64*)malloc(sizeof(u64) * (size_t)l * N);
+        modup_all(c, d + (size_t)2 * L * N, level, up);
+        inner_acc(c, up, rlk, level, 0, acc);
+        u64 srcp[MAXP];
+        for (int k = 0; k < K; k++) srcp[k] = c->prm[L + k];
+        srcp[K] = c->prm[l];
+        u64 hinv[MAXP];
+        double dinv[MAXP];
+        for (int k = 0; k < ns; k++) {
+            u64 m = srcp[k], prod = 1;
+            for (int k2 = 0; k2 < ns; k2++)
+                if (k2 != k) prod = mulm(prod, srcp[k2] % m, m);
+            hinv[k] = invm(prod, m);
+            dinv[k] = 1.0 / (double)m;
+        }
+        for (int bb = 0; bb < 2; bb++) {
+            u64* ab = acc + (size_t)bb * ext * N;
+            for (int i = 0; i < nl; i++) {  /* acc_Q += P * d_bb */
+                u64 q = c->prm[i], pm = pmod(c, i);
+                const u64* dd = d + ((size_t)bb * L + i) * N;
+                for (int n = 0; n < N; n++) ab[(size_t)i * N + n] = addm(ab[(size_t)i * N + n], mulm(pm, dd[n], q), q);
+            }
+            for (int k = 0; k < K; k++) {
+                memcpy(src + (size_t)k * N, ab + (size_t)(nl + k) * N, sizeof(u64) * N);
+                oc_intt(c, src + (size_t)k * N, L + k);
+            }
+            memcpy(src + (size_t)K * N, ab + (size_t)l * N, sizeof(u64) * N);
+            oc_intt(c, src + (size_t)K * N, l);
+            for (int i = 0; i < l; i++) {
+                u64 q = c->prm[i], mm = 1, hm[MAXP];
+                for (int k = 0; k < ns; k++) {
+                    u64 prod = 1;
+                    for (int k2 = 0; k2 < ns; k2++)
+                        if (k2 != k) prod = mulm(prod, srcp[k2] % q, q);
+                    hm[k] = prod;
+                    mm = mulm(mm, srcp[k] % q, q);
+                }
+                u64* o = conv + (size_t)i * N;
+                for (int n = 0; n < N; n++) {
+                    u64 s = 0;
+                    volatile double v = 0.0;
+                    for (int k = 0; k < ns; k++) {
+                        u64 y = mulm(src[(size_t)k * N + n], hinv[k], srcp[k]);
+                        volatile double t = (double)y * dinv[k];
+                        v = v + t;
+                        s = addm(s, mulm(y % q, hm[k], q), q);
+                    }
+                    volatile double vh = v + 0.5;
+                    u64 r = (u64)floor(vh);
+                    o[n] = subm(s, mulm(r % q, mm, q), q);
+                }
+                oc_ntt(c, o, i);
+                u64 minv = invm(mm, q);
+                u64* op = out + (((size_t)x * 2 + bb) * L + i) * N;
+                for (int n = 0; n < N; n++) op[n] = mulm(subm(ab[(size_t)i * N + n], o[n], q), minv, q);
+            }
+        }
+        free(up); free(acc); free(src); free(conv);
+    }
+}
+void oc_mul_relin_rescale(oc_ctx* c, const u64* a, const u64* b, const u64* rlk, u64* out, int count, int level) {
+    int N = c->n, L = c->L;
+#pragma omp parallel for
+    for (int x = 0; x < count; x++) {
+        u64* d = (u64*)malloc(sizeof(u64) * (size_t)3 * L * N);
+        oc_tensor(c, a + (size_t)x * 2 * L * N, b + (size_t)x * 2 * L * N, d, level);
+        oc_relin_rescale_tensor(c, d, rlk, out + (size_t)x * 2 * L * N, level);
+        free(d);
+    }
+}
+
 /* Hoisted rotate-and-sum (device helr_rotsum): out = [a +] sum_t rot_{g_t}(a)
  * with one ModUp of c1, sigma_t applied to the ModUp'd digits, the inner
  * products summed in the extended basis and one ModDown. */

@@ -69,6 +69,8 @@ def lib():
             "oc_keyswitch": (None, [vp, _u64p, _u64p, ctypes.c_int, _u64p, _u64p]),
             "oc_rotsum": (None, [vp, _u64p, ctypes.c_int, _i64p, ctypes.POINTER(_u64p), _u64p, ctypes.c_int,
                                  ctypes.c_int, ctypes.c_int]),
+            "oc_relin_rescale_tensor": (None, [vp, _u64p, _u64p, _u64p, ctypes.c_int]),
+            "oc_mul_relin_rescale": (None, [vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_int, ctypes.c_int]),
             "oc_tensor": (None, [vp, _u64p, _u64p, _u64p, ctypes.c_int]),
             "oc_mul_relin": (None, [vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_int, ctypes.c_int]),
             "oc_automorph": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
@@ -242,6 +244,19 @@ class Oracle:
     def mul_relin(self, a, b, rlk, level):
         out = self._out(a)
         lib().oc_mul_relin(self._h, _p(a), _p(b), _p(rlk), _p(out), a.shape[0], level)
+        return out
+
+    def mul_relin_rescale(self, a, b, rlk, level):
+        """rescale(relin(a*b)) with the rescale merged into ModDown (level-1 out)."""
+        out = self._out(a)
+        lib().oc_mul_relin_rescale(self._h, _p(np.ascontiguousarray(a)), _p(np.ascontiguousarray(b)), _p(rlk),
+                                   _p(out), a.shape[0], level)
+        return out
+
+    def relin_rescale_tensor(self, d, rlk, level):
+        """d = [d0, d1, d2] (u64[3][L][N]) -> one ciphertext at level-1."""
+        out = np.zeros((1, 2, self.L, self.N), dtype=np.uint64)
+        lib().oc_relin_rescale_tensor(self._h, _p(np.ascontiguousarray(d)), _p(rlk), _p(out), level)
         return out
 
     def automorph(self, a, level, galois):

@@ -41,6 +41,17 @@ def _tensor_sum_relin(orc, pairs, rlk, level):
     return out
 
 
+def _tensor_sum_relin_rescale(orc, pairs, rlk, level):
+    """rescale(relin(sum_t a_t (x) b_t)) with the merged ModDown (device
+    op_mul_relin_rescale_sum), output at level-1."""
+    primes = orc.params.q
+    d = None
+    for a, b in pairs:
+        t = orc.tensor(a, b, level)
+        d = t if d is None else _modadd(d, t, level, primes)
+    return orc.relin_rescale_tensor(d, rlk, level)
+
+
 def _galois(k: int, n: int) -> int:
     return pow(5, k % (n // 2), 2 * n)
 
@@ -82,8 +93,7 @@ def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, lo
         rows = []
         for r in range(R):
             # P = Z . W summed over column blocks (enctrain.py:181-183), rescaled
-            prod = _tensor_sum_relin(orc, [(z[r, j][None], w[j][None]) for j in range(C)], rlk, lw)
-            x = orc.rescale(prod, lw)
+            x = _tensor_sum_relin_rescale(orc, [(z[r, j][None], w[j][None]) for j in range(C)], rlk, lw)
             # sum_col_vec left half (hesim.py:255-257)
             if log_baby > 0:
                 x = _bsgs(orc, x, gkeys, log_g, log_baby, +1, lw - 1)
@@ -102,9 +112,9 @@ def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, lo
                     x = orc.rotate(x, ge, gkeys[ge], lw - 2, accumulate=True)
             u = x
             # complement polynomial q0 + q1 u + q2 u^2 + q3 u^3 (enctrain.py:186-191)
-            u2 = orc.rescale(orc.mul_relin(u, u, rlk, lw - 2), lw - 2)
+            u2 = orc.mul_relin_rescale(u, u, rlk, lw - 2)
             tq = orc.rescale(orc.mul_const(u, K[0], lw - 2), lw - 2)
-            qu = orc.rescale(orc.mul_relin(u2, tq, rlk, lw - 3), lw - 3)
+            qu = orc.mul_relin_rescale(u2, tq, rlk, lw - 3)
             lin = orc.rescale(_lincomb(orc, [(u, K[1]), (u2, K[2])], lw - 3), lw - 3)
             qu = orc.add(qu, lin, lw - 4)
             qu = orc.add_const(qu, K[3], lw - 4)
@@ -112,8 +122,7 @@ def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, lo
         # per column block: sum_r qu_r . Z_rj (enctrain.py:193-196 + block sum 374-379)
         gsum = np.zeros((C, 2, orc.L, N), dtype=np.uint64)
         for j in range(C):
-            prod = _tensor_sum_relin(orc, [(rows[r], z[r, j][None]) for r in range(R)], rlk, lw - 4)
-            gsum[j] = orc.rescale(prod, lw - 4)[0]
+            gsum[j] = _tensor_sum_relin_rescale(orc, [(rows[r], z[r, j][None]) for r in range(R)], rlk, lw - 4)[0]
         if phase == 1:
             return gsum
         if phase == 2:
@@ -128,7 +137,7 @@ def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, lo
     # quadratic gradient (enctrain.py:200-208)
     D = np.zeros_like(G)
     for j in range(C):
-        D[j] = orc.rescale(orc.mul_relin(G[j][None], bbar[j][None], rlk, lw - 5), lw - 5)[0]
+        D[j] = orc.mul_relin_rescale(G[j][None], bbar[j][None], rlk, lw - 5)[0]
     # NAG update (enctrain.py:211-239)
     nv = _lincomb(orc, [(w, K[4]), (D, K[5])], lw - 6)
     nw = _lincomb(orc, [(w, K[6]), (v, K[7]), (D, K[8])], lw - 6)

@@ -50,6 +50,7 @@ SIGNATURES = {
     "helr_mul_plain": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_rescale": [_vp, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_relin": [_vp, _u64p, _u64p, _u64p, _u64p, _i, _i, _vp],
+    "helr_mul_relin_rescale": [_vp, _u64p, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_imul": [_vp, _u64p, _u64p, _i, _i, _vp],
     "helr_rotate": [_vp, _u64p, _i64, _u64p, _u64p, _i, _i, _i, _vp],
     "helr_refresh": [_vp, _u64p, _u64p, _i, ctypes.c_double, _u64p, _i, _i, _u64, _u64, _vp],

@@ -327,10 +327,10 @@ class GpuContext:
             else:
                 b = self._drop_to(b, a.level, self.ckks.level_scales[a.level])
         lvl = a.level
-        tmp = self._ct_buffer()
-        self._call("helr_mul_relin", _ptr(a.data), _ptr(b.data), _ptr(self.rlk), _ptr(tmp), 1, lvl, _stream())
         out = self._ct_buffer()
-        self._call("helr_rescale", _ptr(tmp), _ptr(out), 1, lvl, _stream())
+        # tensor, relinearisation and rescale in one key switch (ModDown by P*q_l)
+        self._call("helr_mul_relin_rescale", _ptr(a.data), _ptr(b.data), _ptr(self.rlk), _ptr(out), 1, lvl,
+                   _stream())
         scale = a.scale * b.scale / float(self.ckks.q[lvl])
         return self._wrap(out, lvl - 1, scale, max(a.boot_count, b.boot_count))
 

@@ -202,6 +202,54 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
         double inv = 1.0 / (double)primes[L + k];
         memcpy(&h[o_pid + k], &inv, sizeof(double));
     }
+    // Merged ModDown + rescale by M_l = P * q_l (level l >= 1), source basis
+    // {p_0..p_{K-1}, q_l} -> Q_{l-1}.  Per level, at mr_off[l]:
+    //   [K+1] hinv, [K+1] hinv_sh, [K+1][L] hmod, [K+1][L] hmod_sh,
+    //   [L] M mod q_i, [L] M mod q_i shoup, [L] M^-1 mod q_i, [L] M^-1 shoup, [K+1] 1/m_k (double bits)
+    c->mr_off.assign((size_t)L, 0);
+    for (int l = 1; l < L; l++) {
+        const int ns = K + 1;
+        std::vector<u64> src(ns);
+        for (int k = 0; k < K; k++) src[k] = primes[L + k];
+        src[K] = primes[l];
+        std::vector<u64> e(2 * ns + 2 * (size_t)ns * L + 4 * (size_t)L + ns, 0);
+        u64* hv = e.data();
+        u64* hvs = hv + ns;
+        u64* hm = hvs + ns;
+        u64* hms = hm + (size_t)ns * L;
+        u64* mm = hms + (size_t)ns * L;
+        u64* mms = mm + L;
+        u64* mi = mms + L;
+        u64* mis = mi + L;
+        u64* dinv = mis + L;
+        for (int k = 0; k < ns; k++) {
+            u64 sk = src[k], prod = 1;
+            for (int k2 = 0; k2 < ns; k2++)
+                if (k2 != k) prod = hmul(prod, src[k2] % sk, sk);
+            hv[k] = hinv(prod, sk);
+            hvs[k] = hshoup(hv[k], sk);
+            double inv = 1.0 / (double)sk;
+            memcpy(&dinv[k], &inv, sizeof(double));
+            for (int i = 0; i < l; i++) {
+                u64 qi = primes[i], p2 = 1;
+                for (int k2 = 0; k2 < ns; k2++)
+                    if (k2 != k) p2 = hmul(p2, src[k2] % qi, qi);
+                hm[(size_t)k * L + i] = p2;
+                hms[(size_t)k * L + i] = hshoup(p2, qi);
+            }
+        }
+        for (int i = 0; i < l; i++) {
+            u64 qi = primes[i], m = 1;
+            for (int k = 0; k < ns; k++) m = hmul(m, src[k] % qi, qi);
+            mm[i] = m;
+            mms[i] = hshoup(m, qi);
+            mi[i] = hinv(m, qi);
+            mis[i] = hshoup(mi[i], qi);
+        }
+        size_t o = put(e.size());
+        memcpy(&h[o], e.data(), e.size() * sizeof(u64));
+        c->mr_off[l] = o;
+    }
     // X^(N/2) in NTT form per ciphertext prime (imul)
     size_t o_im = put((size_t)L * n);
     for (int p = 0; p < L; p++)

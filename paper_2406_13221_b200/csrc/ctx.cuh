@@ -46,6 +46,7 @@ struct helr_ctx {
     std::vector<size_t> modup_off;  // [L * beta]
     const u64* modup = nullptr;     // packed, see ctx.cu
     size_t* d_modup_offs = nullptr; // device copy of modup_off
+    std::vector<size_t> mr_off;      // merged ModDown+rescale tables per level (see ctx.cu)
     // ModDown (level-independent)
     const u64* md_phinv = nullptr;     // [K]   (P/p_k)^-1 mod p_k
     const u64* md_phinv_sh = nullptr;

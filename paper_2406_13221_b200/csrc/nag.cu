@@ -112,8 +112,7 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
 
     if (a->phase != 3) {
         // 1) P_r = relin(sum_j Z_rj (x) W_j), rescale -> lw-1
-        TRY(op_mul_relin_sum(c, a->z, (long long)C * CS, CS, a->w, 0, CS, C, a->rlk, T1, CS, R, lw, s));
-        TRY(op_rescale(c, T1, CS, X0, CS, R, lw, s));
+        TRY(op_mul_relin_rescale_sum(c, a->z, (long long)C * CS, CS, a->w, 0, CS, C, a->rlk, X0, CS, R, lw, s));
         // 2) sum_{k<g} rot(P, k): the left half of sum_col_vec (hesim.py:255-257)
         u64* cur = X0;
         u64* nxt = X1;
@@ -145,14 +144,12 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
             }
         }
         // 5) u^2 (lw-3)
-        TRY(op_mul_relin_sum(c, U, CS, 0, U, CS, 0, 1, a->rlk, T1, CS, R, lw - 2, s));
-        TRY(op_rescale(c, T1, CS, U2, CS, R, lw - 2, s));
+        TRY(op_mul_relin_rescale_sum(c, U, CS, 0, U, CS, 0, 1, a->rlk, U2, CS, R, lw - 2, s));
         // 6) q3 u (lw-3)
         TRY(op_ew(c, EW_MULC, U, CS, kc(0), 0, T1, CS, R, lw - 2, s));
         TRY(op_rescale(c, T1, CS, TQ, CS, R, lw - 2, s));
         // 7) u^2 * (q3 u) (lw-4)
-        TRY(op_mul_relin_sum(c, U2, CS, 0, TQ, CS, 0, 1, a->rlk, T1, CS, R, lw - 3, s));
-        TRY(op_rescale(c, T1, CS, QU, CS, R, lw - 3, s));
+        TRY(op_mul_relin_rescale_sum(c, U2, CS, 0, TQ, CS, 0, 1, a->rlk, QU, CS, R, lw - 3, s));
         // 8) + q1 u + q2 u^2 landing on lw-4, + q0
         {
             const u64* xs[2] = {U, U2};
@@ -165,8 +162,7 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
         }
         // 9) G_j = rescale(relin(sum_r QU_r (x) Z_rj))  (lw-5)
         u64* Gdst = (a->phase == 2) ? GT : (a->phase == 1 ? a->grad : G);
-        TRY(op_mul_relin_sum(c, QU, 0, CS, a->z, CS, (long long)C * CS, R, a->rlk, T1, CS, C, lw - 4, s));
-        TRY(op_rescale(c, T1, CS, Gdst, CS, C, lw - 4, s));
+        TRY(op_mul_relin_rescale_sum(c, QU, 0, CS, a->z, CS, (long long)C * CS, R, a->rlk, Gdst, CS, C, lw - 4, s));
         if (a->phase == 2) TRY(op_ew(c, EW_ADD, a->grad, CS, GT, CS, a->grad, CS, C, lw - 5, s));
         if (a->phase != 0) return HELR_OK;
     }
@@ -184,8 +180,7 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
         if (cur != G) cudaMemcpyAsync(G, cur, (size_t)C * CS * sizeof(u64), cudaMemcpyDeviceToDevice, s);
     }
     // 11) D_j = G_j * Bbar_j (enc_quad_gradient, enctrain.py:200-208), lw-6
-    TRY(op_mul_relin_sum(c, G, CS, 0, a->bbar, CS, 0, 1, a->rlk, T1, CS, C, lw - 5, s));
-    TRY(op_rescale(c, T1, CS, D, CS, C, lw - 5, s));
+    TRY(op_mul_relin_rescale_sum(c, G, CS, 0, a->bbar, CS, 0, 1, a->rlk, D, CS, C, lw - 5, s));
     // 12) NAG (enctrain.py:211-239):  V' = W + (1+g) D,  W' = (1-e) V' + e V
     {
         const u64* xv[2] = {a->w, D};

@@ -591,9 +591,12 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
 // inner product: acc[b][poly][e] = sum_j ext[b][j][e] * evk[j][poly][prime(e)]
 // block (64, <= 8): threadIdx.y = ciphertext, so the 8 warps of a block read
 // the same key words (one DRAM read, L1 hits for the rest).
+// dadd (optional): tensor buffer [B][3][L][N]; for Q limbs the accumulator also
+// gets (P mod q) * d0 / d1, so a single division by P*q_l (merged ModDown +
+// rescale) yields rescale(d + KS(d2)).
 __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long ext_digit_stride, const u64* evk,
                            u64* acc, long long acc_item_stride, int n, int nl, int K, int L, int LK, int nd, int B,
-                           Tables tb) {
+                           Tables tb, const u64* dadd, long long dadd_is, const u64* pm, const u64* pm_sh) {
     const int e = blockIdx.y;
     const int b = blockIdx.z * blockDim.y + threadIdx.y;
     const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
@@ -618,8 +621,19 @@ __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long 
         }
     }
     u64* ap = acc + (size_t)b * acc_item_stride;
-    st2(ap + (size_t)e * n + i, barrett128(a00, q, r1, r0), barrett128(a01, q, r1, r0));
-    st2(ap + ((size_t)(nl + K) + e) * n + i, barrett128(a10, q, r1, r0), barrett128(a11, q, r1, r0));
+    u64 o00 = barrett128(a00, q, r1, r0), o01 = barrett128(a01, q, r1, r0);
+    u64 o10 = barrett128(a10, q, r1, r0), o11 = barrett128(a11, q, r1, r0);
+    if (dadd && e < nl) {
+        const u64* db = dadd + (size_t)b * dadd_is + (size_t)e * n + i;
+        const ulonglong2 d0 = ld2(db), d1 = ld2(db + (size_t)L * n);
+        const u64 w = pm[e], ws = pm_sh[e];
+        o00 = add_mod(o00, shoup(d0.x, w, ws, q), q);
+        o01 = add_mod(o01, shoup(d0.y, w, ws, q), q);
+        o10 = add_mod(o10, shoup(d1.x, w, ws, q), q);
+        o11 = add_mod(o11, shoup(d1.y, w, ws, q), q);
+    }
+    st2(ap + (size_t)e * n + i, o00, o01);
+    st2(ap + ((size_t)(nl + K) + e) * n + i, o10, o11);
 }
 
 // ModDown conversion: mdc[b][poly][i] = sum_k [a_k * phinv_k]_{p_k} * phmod[k][i] mod q_i
@@ -831,10 +845,122 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, c
         dim3 g(blocks_for(n / 2, 64), ne, (B + by - 1) / by);
         ProfScope ps(PROF_INNER, 8.0 * n * ((double)B * nd * ne + 2.0 * nd * ne + 2.0 * B * ne), s);
         k_ks_inner<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B,
-                                              c->t);
+                                              c->t, nullptr, 0, nullptr, nullptr);
         CHECK_KERNEL("ks inner");
     }
     return ks_moddown(c, level, ep, B, w, s);
+}
+
+// ---- merged ModDown + rescale --------------------------------------------
+// acc (PQ_l basis, Q limbs already holding acc + P d) -> round(acc / (P q_l))
+// over Q_{l-1}: centred fast conversion from {p_0..p_{K-1}, q_l} (coefficient
+// form) to Q_{l-1}, NTT, then (acc_i - conv_i) * (P q_l)^-1.  Saves the
+// separate rescale's INTT + l NTTs per polynomial.
+struct MrTab {
+    const u64 *hv, *hvs, *hm, *hms, *mm, *mms, *mi, *mis, *dinv;
+};
+static MrTab mr_tab(const helr_ctx* c, int level) {
+    const int ns = c->K + 1, L = c->L;
+    const u64* e = c->d_tab + c->mr_off[level];
+    MrTab t;
+    t.hv = e; t.hvs = e + ns; t.hm = t.hvs + ns; t.hms = t.hm + (size_t)ns * L; t.mm = t.hms + (size_t)ns * L;
+    t.mms = t.mm + L; t.mi = t.mms + L; t.mis = t.mi + L; t.dinv = t.mis + L;
+    return t;
+}
+template <int MK>
+__global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n, int nl,
+                           int K, int L, MrTab mt, Tables tb) {
+    const int it = blockIdx.y;  // item*2 + poly
+    const int b = it >> 1, poly = it & 1;
+    const int ne = nl + K, l = nl - 1, ns = K + 1;
+    const u64* ap = acc + (size_t)b * acc_item_stride + (size_t)poly * ne * n;
+    u64* mp = mdc + (size_t)b * mdc_item_stride + (size_t)poly * L * n;
+    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= n) return;
+    u64 z0[MK], z1[MK];
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < MK; k++) {
+        if (k < ns) {
+            const int lim = k < K ? nl + k : l;
+            const u64 m = tb.q[k < K ? L + k : l];
+            const double inv = __longlong_as_double((long long)mt.dinv[k]);
+            const ulonglong2 x = ld2(ap + (size_t)lim * n + i);
+            z0[k] = shoup(x.x, mt.hv[k], mt.hvs[k], m);
+            z1[k] = shoup(x.y, mt.hv[k], mt.hvs[k], m);
+            v0 = __dadd_rn(v0, __dmul_rn(__ull2double_rn(z0[k]), inv));
+            v1 = __dadd_rn(v1, __dmul_rn(__ull2double_rn(z1[k]), inv));
+        }
+    }
+    const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
+    const u64 rr1 = (u64)__double2ull_rd(__dadd_rn(v1, 0.5));
+    for (int p = 0; p < l; p++) {
+        const u64 q = tb.q[p];
+        u64 s0 = 0, s1 = 0;
+#pragma unroll
+        for (int k = 0; k < MK; k++) {
+            if (k < ns) {
+                const u64 w = mt.hm[(size_t)k * L + p], ws = mt.hms[(size_t)k * L + p];
+                s0 = add_mod(s0, shoup(z0[k], w, ws, q), q);
+                s1 = add_mod(s1, shoup(z1[k], w, ws, q), q);
+            }
+        }
+        st2(mp + (size_t)p * n + i, sub_mod(s0, shoup(rr0, mt.mm[p], mt.mms[p], q), q),
+            sub_mod(s1, shoup(rr1, mt.mm[p], mt.mms[p], q), q));
+    }
+}
+__global__ void k_mdr_final(const u64* acc, long long acc_item_stride, const u64* mdc, long long mdc_item_stride, u64* out,
+                            long long os, int n, int nl, int K, int L, MrTab mt, Tables tb) {
+    const int p = blockIdx.y;
+    const int it = blockIdx.z, b = it >> 1, poly = it & 1;
+    const int ne = nl + K;
+    const u64 q = tb.q[p];
+    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= n) return;
+    const ulonglong2 x = ld2(acc + (size_t)b * acc_item_stride + ((size_t)poly * ne + p) * n + i);
+    const ulonglong2 cv = ld2(mdc + (size_t)b * mdc_item_stride + ((size_t)poly * L + p) * n + i);
+    st2(out + (size_t)b * os + ((size_t)poly * L + p) * n + i, shoup(sub_mod(x.x, cv.x, q), mt.mi[p], mt.mis[p], q),
+        shoup(sub_mod(x.y, cv.y, q), mt.mi[p], mt.mis[p], q));
+}
+
+static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, int B, const KsWs& w, cudaStream_t s) {
+    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K, l = level;
+    MrTab mt = mr_tab(c, level);
+    LimbMap m;
+    m.count = 2 * (K + 1);
+    for (int poly = 0; poly < 2; poly++) {
+        for (int k = 0; k < K; k++) {
+            m.off[poly * (K + 1) + k] = (unsigned char)(poly * ne + nl + k);
+            m.prime[poly * (K + 1) + k] = (unsigned char)(L + k);
+        }
+        m.off[poly * (K + 1) + K] = (unsigned char)(poly * ne + l);
+        m.prime[poly * (K + 1) + K] = (unsigned char)l;
+    }
+    ntt_buffers<true>(c, w.acc, w.acc_s, w.acc, w.acc_s, m, B, s);
+    CHECK_LAUNCH("mdr intt");
+    {
+        dim3 g(blocks_for(n / 2, 128), 2 * B);
+        ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + 1 + l), s);
+        auto conv = K + 1 <= 4 ? k_mdr_conv<4> : (K + 1 <= 8 ? k_mdr_conv<8> : k_mdr_conv<HELR_MAXP>);
+        conv<<<g, 128, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, mt, c->t);
+        CHECK_KERNEL("mdr conv");
+    }
+    LimbMap mq;
+    mq.count = 2 * l;
+    for (int poly = 0; poly < 2; poly++)
+        for (int i = 0; i < l; i++) {
+            mq.off[poly * l + i] = (unsigned char)(poly * L + i);
+            mq.prime[poly * l + i] = (unsigned char)i;
+        }
+    ntt_buffers<false>(c, w.mdc, w.mdc_s, w.mdc, w.mdc_s, mq, B, s);
+    CHECK_LAUNCH("mdr ntt");
+    {
+        dim3 g2(blocks_for(n / 2, 256), l, 2 * B);
+        ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * l * 3.0, s);
+        k_mdr_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, out, os, n, nl, K, L, mt, c->t);
+        CHECK_KERNEL("mdr final");
+    }
+    return HELR_OK;
 }
 
 // ---- hoisted rotate-and-sum ------------------------------------------------
@@ -1029,6 +1155,52 @@ extern "C" int helr_mul_relin(helr_ctx* c, const uint64_t* a, const uint64_t* b,
     const long long cs = 2ll * c->L * c->n;
     return op_mul_relin_sum(c, (const u64*)a, cs, 0, (const u64*)b, cs, 0, 1, (const u64*)rlk, (u64*)out, cs, count,
                             level, S(s));
+}
+
+// out_i (level-1) = rescale(relin(sum_t a (x) b)) with the rescale merged into
+// the key switch's ModDown (one division by P * q_level)
+int op_mul_relin_rescale_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, const u64* b, long long b_is,
+                             long long b_ts, int terms, const u64* rlk, u64* out, long long os, int count, int level,
+                             cudaStream_t s) {
+    if (level < 1 || level >= c->L) { set_error("mul+rescale needs level >= 1"); return HELR_EINVAL; }
+    if (terms < 1) { set_error("need at least one product term"); return HELR_EINVAL; }
+    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
+    const int nd = (nl + c->alpha - 1) / c->alpha;
+    const int chunk = c->max_batch;
+    for (int b0 = 0; b0 < count; b0 += chunk) {
+        int nb = count - b0 < chunk ? count - b0 : chunk;
+        KsWs w = ks_ws(c, chunk);
+        {
+            dim3 g(blocks_for(n, 256), level + 1, nb);
+            ProfScope ps(PROF_TENSOR, 8.0 * n * nb * (level + 1) * (4.0 * terms + 3.0), s);
+            TensorArgs ta{a + (size_t)b0 * a_is, a_is, a_ts, b + (size_t)b0 * b_is, b_is, b_ts, terms};
+            k_tensor<<<g, 256, 0, s>>>(ta, w.tensor, n, L, c->t);
+            CHECK_KERNEL("tensor");
+        }
+        const long long ts = 3ll * L * n;
+        KsInput in{w.tensor + 2ll * L * n, ts, 0};
+        int r = ks_modup(c, in, level, nb, w, s);
+        if (r) return r;
+        {
+            const int by = nb < 8 ? nb : 8;
+            dim3 g(blocks_for(n / 2, 64), ne, (nb + by - 1) / by);
+            ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne + 2.0 * nd * ne + 2.0 * nb * ne + 2.0 * nb * nl), s);
+            k_ks_inner<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, rlk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd,
+                                                  nb, c->t, w.tensor, ts, c->pmod, c->pmod_sh);
+            CHECK_KERNEL("ks inner (+Pd)");
+        }
+        r = ks_moddown_rescale(c, level, out + (size_t)b0 * os, os, nb, w, s);
+        if (r) return r;
+    }
+    return HELR_OK;
+}
+
+extern "C" int helr_mul_relin_rescale(helr_ctx* c, const uint64_t* a, const uint64_t* b, const uint64_t* rlk,
+                                      uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_mul_relin_rescale");
+    const long long cs = 2ll * c->L * c->n;
+    return op_mul_relin_rescale_sum(c, (const u64*)a, cs, 0, (const u64*)b, cs, 0, 1, (const u64*)rlk, (u64*)out, cs,
+                                    count, level, S(s));
 }
 
 int op_rotate(helr_ctx* c, const u64* a, long long as, long long galois, const u64* gk, u64* out, long long os,

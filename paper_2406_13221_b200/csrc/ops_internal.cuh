@@ -22,3 +22,7 @@ int op_lincomb(helr_ctx* c, int terms, const u64* const* x, const long long* xs,
 // products in the extended basis, one ModDown (double hoisting)
 int op_rotsum_hoisted(helr_ctx* c, const u64* a, long long as, int nsteps, const long long* gal, const u64* const* keys,
                       u64* out, long long os, int count, int level, int include_identity, cudaStream_t s);
+// out_i (level-1) = rescale(relin(sum_t a (x) b)), the rescale merged into ModDown
+int op_mul_relin_rescale_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, const u64* b, long long b_is,
+                             long long b_ts, int terms, const u64* rlk, u64* out, long long os, int count, int level,
+                             cudaStream_t s);

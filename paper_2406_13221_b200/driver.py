@@ -160,7 +160,7 @@ class FusedTrainer:
     def __init__(self, ctx: GpuContext, ds, rows_per_block: int, blocks_per_batch: int = 1,
                  mode: str = "mini_batch", poly: PolyApprox = BASELINE_CUBIC, schedule=None,
                  epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False, bsgs: bool = True,
-                 refresh_bits: int = 45):
+                 refresh_bits: int = 47):
         if mode not in ("mini_batch", "full_batch"):
             raise ValueError(f"mode must be mini_batch or full_batch, got {mode!r}")
         from .optimizer import ExpDecay

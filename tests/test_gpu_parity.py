@@ -197,3 +197,17 @@ def test_rotsum_hoisted(pair, rng, steps, ident):
     want = sum(np.roll(z[0], -k) for k in steps) + (z[0] if ident else 0)
     dec = ctx.encoder.decode(orc.decrypt(sk, exp[:1], lvl)[0], cts[0].scale)
     assert np.abs(dec - want).max() < 1e-6
+
+
+def test_mul_relin_rescale_merged(pair, rng):
+    P, ctx, orc, sk = pair
+    _, cts, ref = _fresh(ctx, orc, sk, rng, count=4)
+    rlk = orc.keygen_switch(sk, 0, ctx.key_seed, 0)
+    for lvl in (P.top_level, 1):
+        a = torch.stack([cts[0].data, cts[1].data])
+        b = torch.stack([cts[2].data, cts[3].data])
+        out = ctx._empty((2, 2, P.L, P.n))
+        _lib.call("helr_mul_relin_rescale", ctx.handle, a.data_ptr(), b.data_ptr(), ctx.rlk.data_ptr(),
+                  out.data_ptr(), 2, lvl, stream())
+        exp = orc.mul_relin_rescale(ref[0:2].copy(), ref[2:4].copy(), rlk, lvl)
+        np.testing.assert_array_equal(u64(out)[:, :, :lvl], exp[:, :, :lvl])

@@ -25,13 +25,14 @@ CFG = {
 }
 
 
-def run(name, refresh_bits=45):
+def run(name, refresh_bits=None):
     make, log_n, rows, blocks, mode = CFG[name]
     gold = np.load(ROOT / "tests" / "golden" / f"{name}.npz")
     ds = make()
     ctx = GpuContext(CkksParams.generate(log_n=log_n, n_q=8, dnum=3), seed=2, max_batch=8)
-    tr = FusedTrainer(ctx, ds, rows_per_block=rows, blocks_per_batch=blocks, mode=mode, use_graph=True,
-                      refresh_bits=refresh_bits)
+    kw = {} if refresh_bits is None else dict(refresh_bits=refresh_bits)
+    tr = FusedTrainer(ctx, ds, rows_per_block=rows, blocks_per_batch=blocks, mode=mode, use_graph=True, **kw)
+    refresh_bits = tr.refresh_bits
     its = [int(x) for x in gold["iterations"]]
     worst_w = worst_a = 0.0
     curve = []
@@ -55,4 +56,4 @@ def run(name, refresh_bits=45):
 if __name__ == "__main__":
     for spec in sys.argv[1:] or ["toy", "medium", "paper_mini"]:
         name, _, bits = spec.partition(":")
-        run(name, int(bits) if bits else 45)
+        run(name, int(bits) if bits else None)

@@ -86,6 +86,20 @@ def run(log_n, L, dnum, batch, ops):
         ms = timed(lambda: _lib.call("helr_rotate", ctx.handle, cts.data_ptr(), gal, gk.data_ptr(), out.data_ptr(), batch,
                                      lvl, 0, st))
         res.append(("rotate", ms, (2 * L + 2 * beta * (L + K) + 2 * L) * n * 8 * batch))
+    if "rotsum" in ops:
+        import ctypes
+        steps = list(range(1, 16))
+        gals = [ctx.galois_for_rotation(k) for k in steps]
+        keys = [ctx.galois_key(x) for x in gals]
+        garr = (ctypes.c_int64 * len(gals))(*gals)
+        karr = (ctypes.c_void_p * len(keys))(*[k.data_ptr() for k in keys])
+        lv = min(lvl, 6)
+        ms = timed(lambda: _lib.call("helr_rotsum", ctx.handle, cts.data_ptr(), len(gals), garr, karr, out.data_ptr(),
+                                     batch, lv, 1, st))
+        nl = lv + 1
+        nd = -(-nl // ck.alpha)
+        by = (4 * nl + len(steps) * 2 * nd * (nl + K) / batch + 2 * nd * (nl + K) + 2 * nl) * n * 8 * batch
+        res.append(("rotsum15", ms, by))
     del ctx
     torch.cuda.empty_cache()
     return res
@@ -95,7 +109,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--json", default=None)
-    ap.add_argument("--ops", default="ntt,mul,rescale,rotate")
+    ap.add_argument("--ops", default="ntt,mul,rescale,rotate,rotsum")
     a = ap.parse_args()
     ops = a.ops.split(",")
     P = peak()
