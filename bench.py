@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--workload", choices=list(WORKLOADS), default="paper_mini")
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--cpu-iters", type=int, default=200, help="bounded CPU-baseline sample (iterations)")
+    p.add_argument("--cpu-iters", type=int, default=1000, help="bounded CPU-baseline sample (iterations)")
     p.add_argument("--cpu-rns", action="store_true", help="also time the CPU RNS-CKKS oracle (1 iteration)")
     p.add_argument("--profile-steps", type=int, default=4)
     p.add_argument("--dnum", type=int, default=None, help="override the key-switching digit count")
@@ -156,23 +156,41 @@ def ncu_traffic():
         return {}
 
 
+def max_over_ranks(x: float, ws: int) -> float:
+    """Max of a per-rank device time over all ranks (the slowest replica sets
+    the whole-job time).  Works on nccl (CUDA tensor) and gloo (CPU tensor)."""
+    if ws <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(steps: int, ws: int, ms_max: float) -> float:
+    """Whole-job iterations/s: every replica runs ``steps`` iterations."""
+    return steps * ws / (ms_max / 1000.0)
+
+
 # ----------------------------------------------------------------- reference arm
-def cpu_reference_sample(wl, iters):
+def cpu_reference_sample(wl, iters, warm=0):
     """The reference's own algorithm (slot-level simulator circuit, restated
-    in oracle/slotsim.py) on host cores, bounded to ``iters`` iterations."""
+    in oracle/slotsim.py) on host cores: ``warm`` untimed iterations, then
+    ``iters`` timed ones (dataset encryption excluded).  Returns
+    (iterations/s, timed seconds, timed iterations)."""
     from oracle import slotsim
     from paper_2406_13221_b200.optimizer import BASELINE_CUBIC
     ds = make_dataset(wl["data"])
     qpoly = BASELINE_CUBIC.complement().padded(3)
     mode = wl["mode"]
     if mode == "full_batch":
-        iters = max(1, min(iters, 2))
-    t0 = time.perf_counter()
-    slotsim.train(ds.X, ds.y, wl["log_n"], wl["rows"], wl["blocks"], qpoly, lr_fn, 0, mode=mode, trace=False)
-    t_prep = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    slotsim.train(ds.X, ds.y, wl["log_n"], wl["rows"], wl["blocks"], qpoly, lr_fn, iters, mode=mode, trace=False)
-    dt = time.perf_counter() - t0 - t_prep
+        iters, warm = max(1, min(iters, 2)), min(warm, 1)
+    stamps = []
+    slotsim.train(ds.X, ds.y, wl["log_n"], wl["rows"], wl["blocks"], qpoly, lr_fn, warm + iters, mode=mode,
+                  trace=False, stamps=stamps)
+    dt = stamps[-1] - stamps[warm]
     return iters / dt, dt, iters
 
 
@@ -184,7 +202,7 @@ def run_reference(args, wl, ws, rank):
     from oracle import slotsim  # noqa: F401
     cores = 1  # numpy slot arithmetic is single-threaded
     # warm-up + timed sample, each step one iteration of the reference circuit
-    rate, dt, iters = cpu_reference_sample(wl, steps + warm)
+    rate, dt, iters = cpu_reference_sample(wl, steps, warm)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws, "steps": steps,
         "warmup": warm, "ms_per_step": 1000.0 / rate, "higher_is_better": True, "scaling": "weak",
@@ -192,7 +210,8 @@ def run_reference(args, wl, ws, rank):
         "config": {"workload": args.workload, "n": 422108 if "paper" in args.workload else None,
                    "batch_rows": wl["rows"] * wl["blocks"], "log_n": wl["log_n"], "parallelism": "replicas"},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{iters} iterations of the reference simulator circuit (oracle/slotsim.py)"},
+                         "sample": f"{iters} timed iterations (after {warm} warm-up) of the reference simulator circuit "
+                                   f"(oracle/slotsim.py), {dt:.2f} s"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "epoch_s": 413.0 / rate if "paper" in args.workload else None,
     }
@@ -253,12 +272,8 @@ def main():
     e1.record(stream)
     barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    value = steps * ws / (ms / 1000.0)
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    value = job_throughput(steps, ws, ms)
 
     # ---------------- live per-kernel attribution: CUDA events recorded inside a
     # captured graph (no host launch gaps), one category pair per launch
@@ -307,20 +322,16 @@ def main():
             tr.iterate()
         f1.record(stream)
         barrier()
-        ems = f0.elapsed_time(f1)
-        if ws > 1:
-            t = torch.tensor([ems], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(f0.elapsed_time(f1), ws)
         h2d, d2h = tr.bytes_per_step()
-        e2e = {"value": steps * ws / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": job_throughput(steps, ws, ems), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / steps}
         tr.disable_host_stream()
 
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and args.cpu_iters > 0:
-        rate, dt, iters = cpu_reference_sample(wl, args.cpu_iters)
+        rate, dt, iters = cpu_reference_sample(wl, args.cpu_iters, warm=5)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"{iters} iterations of the reference simulator circuit (oracle/slotsim.py), {dt:.1f} s"}
 

@@ -24,6 +24,7 @@ reference itself from /root/reference).
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -162,8 +163,12 @@ def bbar_of(X, eps=1e-8):
 
 
 def train(X, y, log_n, m, blocks_per_batch, qpoly, lr_fn, iterations, mode="mini_batch", eps=1e-8,
-          log_delta=40, trace=True):
-    """BASELINE recipe over the slot simulator; returns (weights trace, final w)."""
+          log_delta=40, trace=True, stamps=None):
+    """BASELINE recipe over the slot simulator; returns (weights trace, final w).
+
+    ``stamps``: optional list that receives time.perf_counter() at the start
+    of every iteration and once after the last (bench.py's CPU arm times the
+    iterations only, not the encryption of the dataset)."""
     S = 1 << (log_n - 1)
     g = S // m
     sim = SlotSim(log_n, log_q=10 ** 7, log_delta=log_delta, log_delta_c=log_delta)
@@ -186,6 +191,8 @@ def train(X, y, log_n, m, blocks_per_batch, qpoly, lr_fn, iterations, mode="mini
     a1 = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * a0 * a0))
     out = []
     for t in range(iterations):
+        if stamps is not None:
+            stamps.append(time.perf_counter())
         if mode == "mini_batch":
             b = t % nb
             blk = list(range(b * blocks_per_batch, min((b + 1) * blocks_per_batch, rb)))
@@ -214,6 +221,8 @@ def train(X, y, log_n, m, blocks_per_batch, qpoly, lr_fn, iterations, mode="mini
         a0, a1 = a1, 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * a1 * a1))
         if trace:
             out.append(np.concatenate([np.real(c.slots.reshape(m, g)[0]) for c in w])[:cols])
+    if stamps is not None:
+        stamps.append(time.perf_counter())
     final = np.concatenate([np.real(c.slots.reshape(m, g)[0]) for c in w])[:cols]
     return out, final
 

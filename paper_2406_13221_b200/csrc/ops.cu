@@ -14,6 +14,7 @@
 // read once per call (key batching across the row blocks of a mini-batch).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -974,63 +975,220 @@ struct HoistKeys {
     const u64* key[HELR_MAX_HOIST];
     long long gal[HELR_MAX_HOIST];
 };
-struct u192v { u64 lo, mid, hi; };
-__device__ __forceinline__ void mac192(u192v& a, u64 x, u64 y) {
-    const u64 plo = x * y, phi = __umul64hi(x, y);
-    asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, 0;"
-        : "+l"(a.lo), "+l"(a.mid), "+l"(a.hi)
-        : "l"(plo), "l"(phi));
+// One thread per (coefficient i, extended limb e) carries the accumulators of
+// up to NB ciphertexts, so each key word is loaded once per launch chunk and
+// reused NB times from a register, and every step issues 2 nd + NB nd
+// independent loads (memory-level parallelism without high occupancy).
+// Accumulation is 128-bit: every product is < 2^122 (all primes < 2^61), so
+// up to 63 products fit; longer sums fold to a residue every `fold` steps
+// (host-computed from the largest prime, see hoist_fold).
+struct u128acc { u64 lo, hi; };
+// Split accumulator for a sum of 64x64-bit products: lo + hi 2^64 holds
+// sum x0 y0 + x1 y1 2^64, mid (+ carries 2^64) holds sum x0 y1 + x1 y0, so each
+// product costs four 32x32->64 multiply-adds with carry (aligned register
+// pairs, no shuffling) plus one carry count; resolved once per output.
+struct macc { u64 lo, hi, mid; u32 mc; };
+__device__ __forceinline__ void mac_split(macc& a, u64 x, u64 y) {
+    asm("{\n\t"
+        ".reg .u32 x0, x1, y0, y1, a0, a1, a2, a3, m0, m1;\n\t"
+        "mov.b64 {x0, x1}, %4;\n\t"
+        "mov.b64 {y0, y1}, %5;\n\t"
+        "mov.b64 {a0, a1}, %0;\n\t"
+        "mov.b64 {a2, a3}, %1;\n\t"
+        "mov.b64 {m0, m1}, %2;\n\t"
+        "mad.lo.cc.u32 a0, x0, y0, a0;\n\t"
+        "madc.hi.cc.u32 a1, x0, y0, a1;\n\t"
+        "madc.lo.cc.u32 a2, x1, y1, a2;\n\t"
+        "madc.hi.u32 a3, x1, y1, a3;\n\t"
+        "mad.lo.cc.u32 m0, x0, y1, m0;\n\t"
+        "madc.hi.cc.u32 m1, x0, y1, m1;\n\t"
+        "addc.u32 %3, %3, 0;\n\t"
+        "mad.lo.cc.u32 m0, x1, y0, m0;\n\t"
+        "madc.hi.cc.u32 m1, x1, y0, m1;\n\t"
+        "addc.u32 %3, %3, 0;\n\t"
+        "mov.b64 %0, {a0, a1};\n\t"
+        "mov.b64 %1, {a2, a3};\n\t"
+        "mov.b64 %2, {m0, m1};\n\t"
+        "}"
+        : "+l"(a.lo), "+l"(a.hi), "+l"(a.mid), "+r"(a.mc)
+        : "l"(x), "l"(y));
 }
-// (hi 2^128 + mid 2^64 + lo) mod q
-__device__ __forceinline__ u64 reduce192(const u192v& a, u64 q, u64 r1, u64 r0, u64 one_sh, u64 t128, u64 t128_sh) {
-    const u64 mid = shoup(a.mid, 1, one_sh, q);  // mid mod q
-    u64 r = barrett128(u128v{mid, a.lo}, q, r1, r0);
-    if (a.hi) r = add_mod(r, shoup(a.hi, t128, t128_sh, q), q);
+// lo + hi 2^64 + (mid + mc 2^64) 2^32 as a 128-bit value (< 2^128 by the fold bound)
+__device__ __forceinline__ u128acc resolve(const macc& a) {
+    u128acc r{a.lo, a.hi};
+    const u64 add_lo = a.mid << 32;
+    const u64 add_hi = (a.mid >> 32) | ((u64)a.mc << 32);
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r.lo), "+l"(r.hi) : "l"(add_lo), "l"(add_hi));
     return r;
 }
-// All loads of one rotation step are issued before its multiply-accumulates
-// (nd <= MAXD digits held in registers) so each thread keeps ~3*nd loads in
-// flight; two steps are unrolled for more memory-level parallelism.
-template <int MAXD>
-__global__ void k_ks_inner_hoisted(const u64* ext, long long ext_item_stride, long long ext_digit_stride, HoistKeys hk,
-                                   u64* acc, long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK,
-                                   int nd, int B, Tables tb, const u64* one_sh, const u64* t128, const u64* t128_sh) {
-    const int e = blockIdx.z;
-    const int b = blockIdx.y * blockDim.y + threadIdx.y;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B || i >= n) return;
+__device__ __forceinline__ u64 reduce128(const u128acc& a, u64 q, u64 r1, u64 r0, u64 one_sh) {
+    return barrett128(u128v{shoup(a.hi, 1, one_sh, q), a.lo}, q, r1, r0);
+}
+// Per-thread asynchronous prefetch: every thread copies the key words and
+// permuted ext words of rotation step t + S - 1 into its own shared-memory
+// slots (cp.async, 8 bytes each) while it multiplies step t, so the gathers'
+// latency overlaps the arithmetic without holding them in registers.  Each
+// slot is written and read by the same thread, so cp.async.wait_group alone
+// orders them (no block barrier).
+__device__ __forceinline__ void cp_async8(u64* dst, const u64* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int HOIST_T = 128;     // threads per block (coefficients per tile)
+constexpr int HOIST_STAGES = 3;  // steps in flight per thread
+
+// grid: x = coefficient tile * chunks + chunk (chunks of NB ciphertexts share
+// the tile's key words through L2 at the same time), y = extended limb e.
+template <int ND, int NB>
+__global__ void __launch_bounds__(HOIST_T, 3)
+k_ks_inner_hoisted(const u64* __restrict__ ext, long long ext_item_stride, long long ext_digit_stride, HoistKeys hk,
+                   u64* acc, long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK, int B,
+                   int nchunks, int fold, Tables tb, const u64* one_sh) {
+    constexpr int W = (2 + NB) * ND;  // words per thread per stage
+    constexpr int S = HOIST_STAGES;
+    extern __shared__ u64 hsm[];
+    const int tid = threadIdx.x;
+    const int e = blockIdx.y;
+    const int tile = blockIdx.x / nchunks, chunk = blockIdx.x - tile * nchunks;
+    const int i = tile * HOIST_T + tid;
+    const int b0 = chunk * NB;
+    if (i >= n) return;
     const int p = e < nl ? e : L + (e - nl);
-    const u64 q = tb.q[p];
-    u192v a0{0, 0, 0}, a1{0, 0, 0};
-    const u64* xb = ext + (size_t)b * ext_item_stride + (size_t)e * n;
-    const size_t k0off = ((size_t)p) * n + i;             // + j*2*LK*n
+    const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p], osh = one_sh[p];
+    const int nb = B - b0 < NB ? B - b0 : NB;
+    const u64* xb = ext + (size_t)b0 * ext_item_stride + (size_t)e * n;
+    const size_t k0off = ((size_t)p) * n + i;
     const size_t k1off = ((size_t)LK + p) * n + i;
     const size_t kds = (size_t)2 * LK * n;
-#pragma unroll 2
-    for (int t = 0; t < hk.nsteps; t++) {
-        const int src = galois_perm(i, (u64)hk.gal[t], log_n);
-        const u64* kt = hk.key[t];
-        u64 u[MAXD], k0[MAXD], k1[MAXD];
+    auto slot = [&](int stage, int w) -> u64* { return hsm + ((size_t)(stage * W + w) * HOIST_T + tid); };
+    auto issue = [&](int t) {
+        if (t < hk.nsteps) {
+            const int stage = t % S;
+            const int src = galois_perm(i, (u64)hk.gal[t], log_n);
+            const u64* kt = hk.key[t];
 #pragma unroll
-        for (int j = 0; j < MAXD; j++) {
-            if (j < nd) {
-                u[j] = xb[(size_t)j * ext_digit_stride + src];
-                k0[j] = __ldg(kt + (size_t)j * kds + k0off);
-                k1[j] = __ldg(kt + (size_t)j * kds + k1off);
+            for (int j = 0; j < ND; j++) {
+                cp_async8(slot(stage, j), kt + (size_t)j * kds + k0off);
+                cp_async8(slot(stage, ND + j), kt + (size_t)j * kds + k1off);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                if (b < nb) {
+#pragma unroll
+                    for (int j = 0; j < ND; j++)
+                        cp_async8(slot(stage, 2 * ND + b * ND + j),
+                                  xb + (size_t)b * ext_item_stride + (size_t)j * ext_digit_stride + src);
+                }
             }
         }
+        cp_async_commit();  // empty groups keep the wait count uniform
+    };
+    macc a0[NB], a1[NB];
 #pragma unroll
-        for (int j = 0; j < MAXD; j++) {
-            if (j < nd) {
-                mac192(a0, u[j], k0[j]);
-                mac192(a1, u[j], k1[j]);
+    for (int b = 0; b < NB; b++) a0[b] = a1[b] = macc{0, 0, 0, 0};
+#pragma unroll
+    for (int t = 0; t < S - 1; t++) issue(t);
+    int run = 0;
+    for (int t = 0; t < hk.nsteps; t++) {
+        issue(t + S - 1);
+        cp_async_wait<S - 1>();
+        if (run == fold) {  // fold into a residue before the 128-bit sum can overflow
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                a0[b] = macc{reduce128(resolve(a0[b]), q, r1, r0, osh), 0, 0, 0};
+                a1[b] = macc{reduce128(resolve(a1[b]), q, r1, r0, osh), 0, 0, 0};
+            }
+            run = 0;
+        }
+        run++;
+        const int stage = t % S;
+        u64 k0[ND], k1[ND];
+#pragma unroll
+        for (int j = 0; j < ND; j++) {
+            k0[j] = *slot(stage, j);
+            k1[j] = *slot(stage, ND + j);
+        }
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            if (b < nb) {
+#pragma unroll
+                for (int j = 0; j < ND; j++) {
+                    const u64 u = *slot(stage, 2 * ND + b * ND + j);
+                    mac_split(a0[b], u, k0[j]);
+                    mac_split(a1[b], u, k1[j]);
+                }
             }
         }
     }
-    u64* ap = acc + (size_t)b * acc_item_stride;
-    const u64 r1 = tb.br1[p], r0 = tb.br0[p];
-    ap[(size_t)e * n + i] = reduce192(a0, q, r1, r0, one_sh[p], t128[p], t128_sh[p]);
-    ap[((size_t)(nl + K) + e) * n + i] = reduce192(a1, q, r1, r0, one_sh[p], t128[p], t128_sh[p]);
+    cp_async_wait<0>();
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        if (b < nb) {
+            u64* ap = acc + (size_t)(b0 + b) * acc_item_stride;
+            ap[(size_t)e * n + i] = reduce128(resolve(a0[b]), q, r1, r0, osh);
+            ap[((size_t)(nl + K) + e) * n + i] = reduce128(resolve(a1[b]), q, r1, r0, osh);
+        }
+    }
+}
+
+// Steps per 128-bit accumulation run: a run adds fold*nd products (each <
+// 2^(2 bits)) to a residue (< 2^bits) and must stay below 2^128.
+static int hoist_fold(const helr_ctx* c, int nd) {
+    int bits = 0;
+    for (u64 q : c->primes) {
+        int b = 64 - __builtin_clzll(q);
+        if (b > bits) bits = b;
+    }
+    const int room = 128 - 2 * bits;  // 2^room products fit, less one for the residue
+    const long long terms = room >= 20 ? (1ll << 20) : (1ll << room) - 1;
+    const long long f = terms / nd;
+    return f < 1 ? 1 : (f > (1 << 20) ? (1 << 20) : (int)f);
+}
+
+template <int ND, int NB>
+static int launch_hoisted_nb(int nb, dim3 g, cudaStream_t s, const u64* ext, long long es, long long eds,
+                             const HoistKeys& hk, u64* acc, long long as, int n, int log_n, int nl, int K, int L,
+                             int LK, int fold, const Tables& tb, const u64* one_sh) {
+    const int nchunks = (nb + NB - 1) / NB;
+    const size_t smem = sizeof(u64) * (size_t)HOIST_STAGES * (2 + NB) * ND * HOIST_T;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ks_inner_hoisted<ND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    g.x *= nchunks;
+    k_ks_inner_hoisted<ND, NB><<<g, HOIST_T, smem, s>>>(ext, es, eds, hk, acc, as, n, log_n, nl, K, L, LK, nb, nchunks,
+                                                        fold, tb, one_sh);
+    return 0;
+}
+// ciphertexts per thread: HELR_HOIST_NB (1, 2, 4 or 8; default 4) caps it
+static int hoist_nb_cap() {
+    static int cap = -1;
+    if (cap < 0) {
+        const char* v = getenv("HELR_HOIST_NB");
+        cap = v ? atoi(v) : 4;
+        if (cap != 1 && cap != 2 && cap != 8) cap = 4;
+    }
+    return cap;
+}
+template <int ND>
+static void launch_hoisted(int nb, dim3 g, cudaStream_t s, const u64* ext, long long es, long long eds,
+                           const HoistKeys& hk, u64* acc, long long as, int n, int log_n, int nl, int K, int L, int LK,
+                           int fold, const Tables& tb, const u64* one_sh) {
+    const int cap = hoist_nb_cap();
+    const int want = nb <= 1 ? 1 : nb <= 2 ? 2 : nb <= 4 ? 4 : 8;
+    const int NBs = want < cap ? want : cap;
+#define HELR_HNB(V) launch_hoisted_nb<ND, V>(nb, g, s, ext, es, eds, hk, acc, as, n, log_n, nl, K, L, LK, fold, tb, one_sh)
+    if (NBs == 1) HELR_HNB(1);
+    else if (NBs == 2) HELR_HNB(2);
+    else if (NBs == 4) HELR_HNB(4);
+    else if constexpr (ND <= 3) HELR_HNB(8);
+    else HELR_HNB(4);
+#undef HELR_HNB
 }
 
 int op_rotsum_hoisted(helr_ctx* c, const u64* a, long long as, int nsteps, const long long* gal, const u64* const* keys,
@@ -1064,12 +1222,23 @@ int op_rotsum_hoisted(helr_ctx* c, const u64* a, long long as, int nsteps, const
         int r = ks_modup(c, in, level, nb, w, s);
         if (r) return r;
         {
-            const int by = nb < 4 ? nb : 4;
-            dim3 g(blocks_for(n, 64), (nb + by - 1) / by, ne);
+            dim3 g(blocks_for(n, HOIST_T), ne, 1);
+            const int fold = hoist_fold(c, nd);
             ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne * nsteps + 2.0 * nd * ne * nsteps + 2.0 * nb * ne), s);
-            auto kern = nd <= 4 ? k_ks_inner_hoisted<4> : (nd <= 8 ? k_ks_inner_hoisted<8> : k_ks_inner_hoisted<32>);
-            kern<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, hk, w.acc, w.acc_s, n, c->log_n, nl, K, L, c->LK,
-                                            nd, nb, c->t, c->one_sh, c->t128, c->t128_sh);
+#define HELR_HND(D) launch_hoisted<D>(nb, g, s, w.ext, w.ext_s, w.ext_ds, hk, w.acc, w.acc_s, n, c->log_n, nl, K, L, \
+                                     c->LK, fold, c->t, c->one_sh)
+            switch (nd) {
+                case 1: HELR_HND(1); break;
+                case 2: HELR_HND(2); break;
+                case 3: HELR_HND(3); break;
+                case 4: HELR_HND(4); break;
+                case 5: HELR_HND(5); break;
+                case 6: HELR_HND(6); break;
+                case 7: HELR_HND(7); break;
+                case 8: HELR_HND(8); break;
+                default: set_error("rotsum: more than 8 key-switching digits"); return HELR_EINVAL;
+            }
+#undef HELR_HND
             CHECK_KERNEL("rotsum inner");
         }
         KsEpilogue ep = make_epilogue(out + (size_t)b0 * os, os, include_identity ? ab : nullptr, as, ab, as, nsteps, gg);
