@@ -198,6 +198,7 @@ class FusedTrainer:
         self.host_stream = False
         self.z_host = None
         self.b_host = None
+        self.copy_stream = None
         self._prepare()
 
     # ------------------------------------------------------------ client side
@@ -278,12 +279,25 @@ class FusedTrainer:
 
     def enable_host_stream(self):
         """Keep the encrypted dataset in pinned host memory and stream each
-        batch to the device inside the iteration (the e2e path)."""
+        batch to the device inside the iteration (the e2e path).
+
+        Copies are double-buffered on a separate copy stream: while iteration
+        t runs on staging buffer t % 2, the host-to-device copy of the next
+        batch fills the other buffer (event-ordered both ways), so the PCIe
+        transfer overlaps the encrypted arithmetic."""
         if self.z_host is None:
             self.z_host = torch.empty(self.z.shape, dtype=torch.int64, pin_memory=True)
             self.z_host.copy_(self.z)
             self.b_host = torch.empty(self.bbar.shape, dtype=torch.int64, pin_memory=True)
             self.b_host.copy_(self.bbar)
+        if self.copy_stream is None:
+            self.copy_stream = torch.cuda.Stream(device=self.ctx.device)
+            self._zst = [self.zstage, torch.empty_like(self.zstage)]
+            self._bst = [self.bstage, torch.empty_like(self.bstage)]
+        self._buf = 0
+        self._loaded = [None, None]   # (batch, bbar index) each buffer holds / is receiving
+        self._ready = [None, None]    # copy finished (copy stream)
+        self._free = [None, None]     # last reader finished (compute stream)
         self.host_stream = True
 
     def disable_host_stream(self):
@@ -339,11 +353,12 @@ class FusedTrainer:
         self.level = top
         self.s_w = self.s_v = target
 
-    def _args(self, plan: IterPlan, phase: int) -> NagArgs:
+    def _args(self, plan: IterPlan, phase: int, zb=None) -> NagArgs:
         C = self.cols
         cs = self.wv[0].numel() * 8
-        return NagArgs(z=self.zstage.data_ptr(), rows=self.rows, cols=C, log_g=self.log_g, log_m=self.log_m,
-                       w=self.wv.data_ptr(), v=self.wv.data_ptr() + C * cs, bbar=self.bstage.data_ptr(),
+        z_ptr, b_ptr = zb if zb is not None else (self.zstage.data_ptr(), self.bstage.data_ptr())
+        return NagArgs(z=z_ptr, rows=self.rows, cols=C, log_g=self.log_g, log_m=self.log_m,
+                       w=self.wv.data_ptr(), v=self.wv.data_ptr() + C * cs, bbar=b_ptr,
                        lw=plan.lw, rlk=self.ctx.rlk.data_ptr(), rot_left=self._k_left, rot_right=self._k_right,
                        rot_rows=self._k_rows, mask_pt=self._mask(plan.lw, plan.mask_scale).data_ptr(),
                        consts=self.consts_dev.data_ptr(), grad=self.grad.data_ptr(), phase=phase,
@@ -362,11 +377,42 @@ class FusedTrainer:
         self._cev[i] = ev
 
     def _stage(self, batch: int, bbar_index: int, with_bbar: bool = True):
-        src_z = self.z_host if self.host_stream else self.z
-        src_b = self.b_host if self.host_stream else self.bbar
-        self.zstage.copy_(src_z[batch], non_blocking=True)
-        if with_bbar:
-            self.bstage.copy_(src_b[bbar_index], non_blocking=True)
+        """Make (batch, bbar_index) resident in a staging buffer; returns the
+        (z, bbar) device pointers the iteration reads."""
+        if not self.host_stream:
+            self.zstage.copy_(self.z[batch], non_blocking=True)
+            if with_bbar:
+                self.bstage.copy_(self.bbar[bbar_index], non_blocking=True)
+            return self.zstage.data_ptr(), self.bstage.data_ptr()
+        buf = self._buf
+        if self._loaded[buf] is None or self._loaded[buf][0] != batch or self._loaded[buf][1] != bbar_index:
+            self._prefetch(buf, batch, bbar_index)
+        self.stream.wait_event(self._ready[buf])
+        return self._zst[buf].data_ptr(), self._bst[buf].data_ptr()
+
+    def _prefetch(self, buf: int, batch: int, bbar_index: int):
+        cs = self.copy_stream
+        if self._free[buf] is not None:
+            cs.wait_event(self._free[buf])
+        prev = self._loaded[buf]
+        with torch.cuda.stream(cs):
+            self._zst[buf].copy_(self.z_host[batch], non_blocking=True)
+            if prev is None or prev[1] != bbar_index:
+                self._bst[buf].copy_(self.b_host[bbar_index], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self._ready[buf] = ev
+        self._loaded[buf] = (batch, bbar_index)
+
+    def _release(self, next_batch: int, next_bbar: int):
+        """The current buffer's reader is enqueued: mark it, flip buffers and
+        start copying the next batch into the other one."""
+        buf = self._buf
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        self._free[buf] = ev
+        self._buf = 1 - buf
+        self._prefetch(self._buf, next_batch, next_bbar)
 
     def _run(self, args: NagArgs):
         stream = torch.cuda.current_stream().cuda_stream
@@ -375,7 +421,7 @@ class FusedTrainer:
             _lib.check(self.lib.helr_nag_iteration(self.ctx.handle, ctypes.byref(args), stream), "helr_nag_iteration")
             self._warm = True
             return
-        key = (args.lw, args.phase, args.mask_pt)
+        key = (args.lw, args.phase, args.mask_pt, args.z, args.bbar)
         g = self._graphs.get(key)
         if g is None:
             g = ctypes.c_void_p()
@@ -421,14 +467,23 @@ class FusedTrainer:
         lr, eta, gamma, mult = self.step_scalars(self.t, gamma_rows)
         plan = plan_iteration(self.ck, self.level, self.s_w, self.s_v, self.s_z, self.s_b, self.qpoly, mult, eta)
         self._upload_consts(plan)
+        nbt = self.n_batches
         if self.mode == "mini_batch":
-            self._stage(b, b)
-            self._run(self._args(plan, 0))
+            zb = self._stage(b, b)
+            self._run(self._args(plan, 0, zb))
+            if self.host_stream:
+                self._release((b + 1) % nbt, (b + 1) % nbt)
         else:
-            for bb in range(self.n_batches):
-                self._stage(bb, 0, with_bbar=(bb == 0))
-                self._run(self._args(plan, 1 if bb == 0 else 2))
-            self._run(self._args(plan, 3))
+            for bb in range(nbt):
+                zb = self._stage(bb, 0, with_bbar=(bb == 0))
+                self._run(self._args(plan, 1 if bb == 0 else 2, zb))
+                if self.host_stream:
+                    self._release((bb + 1) % nbt, 0)
+            self._run(self._args(plan, 3, zb))
+            if self.host_stream:  # the finish phase reads the last buffer's B̄ too
+                ev = torch.cuda.Event()
+                ev.record(self.stream)
+                self._free[1 - self._buf] = ev
         level_start = self.level
         self.level -= ITER_DEPTH
         self.s_w = self.s_v = plan.s_out

@@ -61,3 +61,25 @@ def test_paper_mini_first_iterations():
     w, a = _run("paper_mini", data.paper_dataset(), 16, 128, 8, "mini_batch", 16, use_graph=True)
     print(f"paper_mini: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
     assert w < TOL and a < TOL
+
+
+@pytest.mark.parametrize("mode,blocks", [("mini_batch", 1), ("full_batch", 4)])
+def test_host_streamed_equals_device_resident(mode, blocks):
+    """The e2e path (pinned host dataset, double-buffered H2D copies on a side
+    stream, graphs keyed per staging buffer) leaves bit-identical W, V
+    ciphertexts to the HBM-resident path."""
+    ds = data.toy_dataset()
+    ck = CkksParams.generate(log_n=13, n_q=8, dnum=3)
+    outs = []
+    for host in (False, True):
+        ctx = GpuContext(ck, seed=2, max_batch=8)
+        tr = FusedTrainer(ctx, ds, rows_per_block=16, blocks_per_batch=blocks, mode=mode, use_graph=True)
+        if host:
+            tr.enable_host_stream()
+        for _ in range(9):
+            tr.iterate()
+        torch.cuda.synchronize()
+        outs.append(tr.wv.cpu().numpy())
+        tr.close()
+    assert tr.n_batches >= 2
+    np.testing.assert_array_equal(outs[0], outs[1])
