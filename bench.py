@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--cpu-rns", action="store_true", help="also time the CPU RNS-CKKS oracle (1 iteration)")
     p.add_argument("--profile-steps", type=int, default=4)
     p.add_argument("--dnum", type=int, default=None, help="override the key-switching digit count")
+    p.add_argument("--bsgs-bits", type=int, default=None, help="max bits per hoisted group (sum_col_vec)")
+    p.add_argument("--rows-bits", type=int, default=None, help="max bits per hoisted group (sum_rows)")
     return p.parse_args()
 
 
@@ -246,7 +248,7 @@ def main():
     ctx = GpuContext(ck, seed=1, max_batch=max(8, wl["blocks"]))
     ds = make_dataset(wl["data"])
     tr = FusedTrainer(ctx, ds, rows_per_block=wl["rows"], blocks_per_batch=wl["blocks"], mode=wl["mode"],
-                      use_graph=not args.no_graph)
+                      use_graph=not args.no_graph, bsgs_bits=args.bsgs_bits, rows_bits=args.rows_bits)
     setup_s = time.perf_counter() - t_setup
     steps = args.steps if args.steps is not None else tr.n_batches
     warm = max(3, args.warmup)
@@ -344,7 +346,7 @@ def main():
                        "padded_cols": tr.layout.col_blocks * tr.layout.g, "log_n": ck.log_n, "L": ck.L,
                        "K": ck.K, "dnum": ck.dnum, "batch_rows": tr.batch_rows, "cts_per_batch": tr.rows,
                        "batches": tr.n_batches, "mode": wl["mode"], "parallelism": "replicas",
-                       "cuda_graph": tr.use_graph,
+                       "cuda_graph": tr.use_graph, "rotsum_group_bits": tr.log_baby, "rows_group_bits": tr.log_baby_rows,
                        "l2": "no flush needed: each step streams a new 64 MiB batch and ~830 MB of keys"},
             "epoch_s": tr.n_batches / (value / ws),
             "hbm_gbs_step": step_gb / (ms / steps / 1000.0),

@@ -188,7 +188,8 @@ typedef struct helr_nag_args {
     const uint64_t* rlk;    /* relinearisation key */
     const uint64_t* const* rot_left;   /* [log_g] keys, left rotation by 2^i */
     const uint64_t* const* rot_right;  /* [log_g] keys, right rotation by 2^i */
-    const uint64_t* const* rot_rows;   /* [log_m] keys, left rotation by g*2^i */
+    const uint64_t* const* rot_rows;   /* [log_m] keys, left rotation by g*2^i
+                                          (or grouped, see log_baby_rows) */
     const uint64_t* mask_pt;           /* [L][N] row-start mask plaintext (NTT) */
     const uint64_t* consts;            /* device [HELR_NAG_NCONST][L] */
     uint64_t* grad;                    /* [cols] gradient accumulator (full batch) */
@@ -196,11 +197,21 @@ typedef struct helr_nag_args {
                    2: grad += this batch's gradient; 3: finish from grad (row sums,
                    Bbar product, update) */
     int log_baby; /* 0: sum_col_vec by log2(g) rotate-and-add steps (rot_left[i] /
-                     rot_right[i] rotate by 2^i); bs > 0: baby-step/giant-step with
-                     two hoisted groups per half, rot_left = keys for rotations
-                     1..2^bs-1 then 2^bs*(1..2^(log_g-bs)-1), rot_right likewise
-                     for the negated steps */
+                     rot_right[i] rotate by 2^i); b > 0: hoisted groups of at most b
+                     bits each (helr_rotsum_groups: ceil(log_g / b) groups, bits
+                     spread evenly, larger groups first); group j with offset
+                     o_j = bits of the groups before it sums rotations
+                     k*2^o_j, k = 1..2^bits_j - 1; rot_left holds the keys of
+                     group 0, then group 1, ...; rot_right likewise for the
+                     negated steps */
+    int log_baby_rows; /* sum_rows: 0 = log_m rotate-and-add steps by g*2^i;
+                          b > 0: grouped as above over log_m, steps scaled by g */
 } helr_nag_args;
+
+/* Group bit-widths of a grouped rotate-and-sum over 2^log_total rotations
+ * with groups of at most max_bits bits: returns the number of groups and
+ * writes the widths to bits[] (at most 64 entries). */
+int helr_rotsum_groups(int log_total, int max_bits, int* bits);
 
 int helr_nag_iteration(helr_ctx* ctx, const helr_nag_args* args, void* stream);
 

@@ -65,22 +65,39 @@ def _lincomb(orc, terms, level):
     return acc
 
 
-def _bsgs(orc, x, gkeys, log_g, bs, sign, level):
-    """sum_{k < 2^log_g} rot(x, sign k) as two hoisted groups (helr_rotsum):
-    baby steps 1..2^bs-1, then giant steps 2^bs (1..2^gs-1)."""
+def rotsum_groups(log_total: int, max_bits: int) -> list:
+    """Group bit-widths of a grouped rotate-and-sum (helr_rotsum_groups in
+    csrc/nag.cu): ceil(log_total / max_bits) groups, bits spread evenly,
+    larger groups first."""
+    if log_total <= 0 or max_bits <= 0:
+        return []
+    ng = -(-log_total // max_bits)
+    base, rem = divmod(log_total, ng)
+    return [base + 1 if j < rem else base for j in range(ng)]
+
+
+def grouped_steps(log_total: int, max_bits: int, stride: int = 1) -> list:
+    """Rotation steps of every group, in key order."""
+    out, off = [], 0
+    for bits in rotsum_groups(log_total, max_bits):
+        out.append([(stride * k) << off for k in range(1, 1 << bits)])
+        off += bits
+    return out
+
+
+def _bsgs(orc, x, gkeys, log_g, bs, sign, level, stride=1):
+    """sum_{k < 2^log_g} rot(x, sign stride k) as grouped hoisted rotate-and-sums
+    (helr_rotsum, one ModUp / ModDown per group)."""
     N = orc.N
-    bs = min(bs, log_g)
-    gs = log_g - bs
-    baby = [_galois(sign * k, N) for k in range(1, 1 << bs)]
-    x = orc.rotsum(np.ascontiguousarray(x), baby, [gkeys[g] for g in baby], level, include_identity=True)
-    if gs:
-        giant = [_galois(sign * (k << bs), N) for k in range(1, 1 << gs)]
-        x = orc.rotsum(x, giant, [gkeys[g] for g in giant], level, include_identity=True)
+    x = np.ascontiguousarray(x)
+    for steps in grouped_steps(log_g, bs, stride):
+        gal = [_galois(sign * k, N) for k in steps]
+        x = orc.rotsum(x, gal, [gkeys[g] for g in gal], level, include_identity=True)
     return x
 
 
 def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, log_m, phase=0, grad=None,
-                  log_baby=0):
+                  log_baby=0, log_baby_rows=0):
     """z: u64[R][C][2][L][N]; w, v, bbar, grad: u64[C][2][L][N];
     gkeys: galois element -> key; consts: u64[10][L].
     Returns (w', v') for phase 0, the gradient for phases 1/2, (w', v') for 3."""
@@ -131,9 +148,12 @@ def nag_iteration(orc, z, w, v, bbar, lw, rlk, gkeys, mask_pt, consts, log_g, lo
     else:
         G = grad
     # sum_rows on the batch total (hesim.py:278-280)
-    for i in range(log_m):
-        ge = _galois(g << i, N)
-        G = orc.rotate(np.ascontiguousarray(G), ge, gkeys[ge], lw - 5, accumulate=True)
+    if log_baby_rows > 0:
+        G = _bsgs(orc, G, gkeys, log_m, log_baby_rows, +1, lw - 5, stride=g)
+    else:
+        for i in range(log_m):
+            ge = _galois(g << i, N)
+            G = orc.rotate(np.ascontiguousarray(G), ge, gkeys[ge], lw - 5, accumulate=True)
     # quadratic gradient (enctrain.py:200-208)
     D = np.zeros_like(G)
     for j in range(C):

@@ -54,6 +54,7 @@ SIGNATURES = {
     "helr_imul": [_vp, _u64p, _u64p, _i, _i, _vp],
     "helr_rotate": [_vp, _u64p, _i64, _u64p, _u64p, _i, _i, _i, _vp],
     "helr_refresh": [_vp, _u64p, _u64p, _i, ctypes.c_double, _u64p, _i, _i, _u64, _u64, _vp],
+    "helr_rotsum_groups": [_i, _i, ctypes.POINTER(ctypes.c_int)],
     "helr_rotsum": [_vp, _u64p, _i, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p), _u64p, _i, _i, _i,
                     _vp],
     "helr_nag_iteration": None,  # bound lazily by driver.py (struct argument)

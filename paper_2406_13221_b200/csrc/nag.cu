@@ -60,26 +60,50 @@ static long long pow_mod_ll(long long b, long long e, long long m) {
     return r;
 }
 
-// sum_{k < 2^log_g} rot(x, sign*k) by baby-step/giant-step: two hoisted
-// rotate-and-sum groups (baby 1..2^bs-1, giant 2^bs*(1..2^gs-1)), each with one
-// ModUp and one ModDown.  keys: baby keys then giant keys.  `in` is clobbered
-// as scratch; the result lands in `out`.
-static int bsgs_rotsum(helr_ctx* c, const uint64_t* const* keys, int log_g, int bs, int sign, u64* in, u64* out, int R,
-                       int level, cudaStream_t s) {
+extern "C" int helr_rotsum_groups(int log_total, int max_bits, int* bits) {
+    if (log_total <= 0 || max_bits <= 0) return 0;
+    const int ng = (log_total + max_bits - 1) / max_bits;
+    const int base = log_total / ng, rem = log_total % ng;
+    for (int j = 0; j < ng && j < 64; j++) bits[j] = base + (j < rem ? 1 : 0);
+    return ng;
+}
+
+// out = sum_{k < 2^log_total} rot(in, sign * stride * k) as grouped hoisted
+// rotate-and-sums (helr_rotsum_groups): group j sums rotations
+// stride * k * 2^off_j, k = 1..2^bits_j - 1, plus the identity, with one ModUp
+// and one ModDown per group.  keys: group 0's keys, then group 1's, ...
+// `tmp` is scratch; `out` may alias `in`, neither may alias `tmp`.
+static int grouped_rotsum(helr_ctx* c, const uint64_t* const* keys, int log_total, int max_bits, int sign,
+                          long long stride, const u64* in, u64* out, u64* tmp, int R, int level, cudaStream_t s) {
     const long long CS = 2ll * c->L * c->n, two_n = 2ll * c->n, slots = c->n / 2;
-    if (bs > log_g) bs = log_g;
-    const int gs = log_g - bs;
-    const int nb = (1 << bs) - 1, ng = (1 << gs) - 1;
-    long long gal[64];
-    for (int k = 1; k <= nb; k++) gal[k - 1] = pow_mod_ll(5, sign > 0 ? k : slots - k, two_n);
-    if (ng == 0) return op_rotsum_hoisted(c, in, CS, nb, gal, (const u64* const*)keys, out, CS, R, level, 1, s);
-    TRY(op_rotsum_hoisted(c, in, CS, nb, gal, (const u64* const*)keys, out, CS, R, level, 1, s));
-    for (int k = 1; k <= ng; k++) {
-        const long long step = (long long)k << bs;
-        gal[k - 1] = pow_mod_ll(5, sign > 0 ? step : slots - step, two_n);
+    int bits[64];
+    const int ng = helr_rotsum_groups(log_total, max_bits, bits);
+    if (ng == 0) {
+        if (out != in) cudaMemcpyAsync(out, in, (size_t)R * CS * sizeof(u64), cudaMemcpyDeviceToDevice, s);
+        return HELR_OK;
     }
-    TRY(op_rotsum_hoisted(c, out, CS, ng, gal, (const u64* const*)(keys + nb), in, CS, R, level, 1, s));
-    cudaMemcpyAsync(out, in, (size_t)R * CS * sizeof(u64), cudaMemcpyDeviceToDevice, s);
+    // ping-pong so that the last group writes `out`
+    const u64* src = in;
+    int off = 0, kbase = 0;
+    for (int j = 0; j < ng; j++) {
+        u64* dst = ((ng - 1 - j) % 2 == 0) ? out : tmp;
+        if (dst == src) dst = (dst == out) ? tmp : out;  // never alias a group's input
+        const int nk = (1 << bits[j]) - 1;
+        if (nk > HELR_MAX_HOIST) {
+            set_error("grouped rotsum: at most 5 bits (31 rotations) per hoisted group");
+            return HELR_EINVAL;
+        }
+        long long gal[HELR_MAX_HOIST];
+        for (int k = 1; k <= nk; k++) {
+            const long long step = ((stride * (long long)k) << off) % slots;
+            gal[k - 1] = pow_mod_ll(5, sign > 0 ? step : (slots - step) % slots, two_n);
+        }
+        TRY(op_rotsum_hoisted(c, src, CS, nk, gal, (const u64* const*)(keys + kbase), dst, CS, R, level, 1, s));
+        src = dst;
+        off += bits[j];
+        kbase += nk;
+    }
+    if (src != out) cudaMemcpyAsync(out, src, (size_t)R * CS * sizeof(u64), cudaMemcpyDeviceToDevice, s);
     return HELR_OK;
 }
 
@@ -117,7 +141,7 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
         u64* cur = X0;
         u64* nxt = X1;
         if (a->log_baby > 0) {
-            TRY(bsgs_rotsum(c, a->rot_left, a->log_g, a->log_baby, +1, cur, nxt, R, lw - 1, s));
+            TRY(grouped_rotsum(c, a->rot_left, a->log_g, a->log_baby, +1, 1, cur, nxt, T1, R, lw - 1, s));
             u64* t = cur; cur = nxt; nxt = t;
         } else {
             for (int i = 0; i < a->log_g; i++) {
@@ -131,7 +155,7 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
         TRY(op_rescale(c, T1, CS, cur, CS, R, lw - 1, s));
         // 4) sum_{k<g} rot(M, -k): the right half (hesim.py:262-264)
         if (a->log_baby > 0) {
-            TRY(bsgs_rotsum(c, a->rot_right, a->log_g, a->log_baby, -1, cur, U, R, lw - 2, s));
+            TRY(grouped_rotsum(c, a->rot_right, a->log_g, a->log_baby, -1, 1, cur, U, T1, R, lw - 2, s));
         } else {
             for (int i = 0; i < a->log_g; i++) {
                 const long long g = pow_mod_ll(5, slots - (1ll << i), two_n);
@@ -168,7 +192,10 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
     }
     const u64* Gsrc = (a->phase == 3) ? a->grad : G;
     // 10) sum_rows: rotate-and-add by g, 2g, ..., (m/2) g (hesim.py:278-280)
-    {
+    if (a->log_baby_rows > 0) {
+        TRY(grouped_rotsum(c, a->rot_rows, a->log_m, a->log_baby_rows, +1, 1ll << a->log_g, Gsrc, G, GT, C, lw - 5,
+                           s));
+    } else {
         const u64* cur = Gsrc;
         u64* bufs[2] = {GT, D};
         for (int i = 0; i < a->log_m; i++) {

@@ -498,7 +498,6 @@ struct KsInput {
     long long d_stride;
     long long galois;    // 0: none, else apply X -> X^galois to d first
 };
-#define HELR_MAX_HOIST 32
 struct KsEpilogue {
     u64* out;             // ciphertext of item b at out + b*out_stride
     long long out_stride;

@@ -3,6 +3,9 @@
 // Strides are in 64-bit words between consecutive ciphertexts; a stride of 0
 // broadcasts one ciphertext to every item.
 #pragma once
+
+// rotations per hoisted rotate-and-sum group (op_rotsum_hoisted)
+#define HELR_MAX_HOIST 32
 #include "ctx.cuh"
 
 enum EwOp { EW_ADD = 0, EW_SUB, EW_ADDC, EW_ADDPT, EW_MULC, EW_MULPT, EW_IMUL };

@@ -39,6 +39,25 @@ NCONST = 10
 ITER_DEPTH = 7  # rescales per iteration
 
 
+def rotsum_groups(log_total: int, max_bits: int) -> list:
+    """Bit-widths of the hoisted groups of a grouped rotate-and-sum over
+    2^log_total rotations (same rule as helr_rotsum_groups, csrc/nag.cu)."""
+    if log_total <= 0 or max_bits <= 0:
+        return []
+    ng = -(-log_total // max_bits)
+    base, rem = divmod(log_total, ng)
+    return [base + 1 if j < rem else base for j in range(ng)]
+
+
+def grouped_steps(log_total: int, max_bits: int, stride: int = 1) -> list:
+    """Rotation steps per group (key order of helr_nag_args.rot_*)."""
+    out, off = [], 0
+    for bits in rotsum_groups(log_total, max_bits):
+        out.append([(stride * k) << off for k in range(1, 1 << bits)])
+        off += bits
+    return out
+
+
 class NagArgs(ctypes.Structure):
     """Mirror of ``helr_nag_args`` (include/helr_ckks.h)."""
 
@@ -50,7 +69,7 @@ class NagArgs(ctypes.Structure):
         ("rot_left", ctypes.POINTER(ctypes.c_void_p)), ("rot_right", ctypes.POINTER(ctypes.c_void_p)),
         ("rot_rows", ctypes.POINTER(ctypes.c_void_p)),
         ("mask_pt", ctypes.c_void_p), ("consts", ctypes.c_void_p), ("grad", ctypes.c_void_p),
-        ("phase", ctypes.c_int), ("log_baby", ctypes.c_int),
+        ("phase", ctypes.c_int), ("log_baby", ctypes.c_int), ("log_baby_rows", ctypes.c_int),
     ]
 
 
@@ -160,7 +179,7 @@ class FusedTrainer:
     def __init__(self, ctx: GpuContext, ds, rows_per_block: int, blocks_per_batch: int = 1,
                  mode: str = "mini_batch", poly: PolyApprox = BASELINE_CUBIC, schedule=None,
                  epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False, bsgs: bool = True,
-                 refresh_bits: int = 47):
+                 refresh_bits: int = 47, bsgs_bits: Optional[int] = None, rows_bits: Optional[int] = None):
         if mode not in ("mini_batch", "full_batch"):
             raise ValueError(f"mode must be mini_batch or full_batch, got {mode!r}")
         from .optimizer import ExpDecay
@@ -185,8 +204,20 @@ class FusedTrainer:
         self.log_g = int(math.log2(lay.g))
         self.log_m = int(math.log2(lay.m))
         self.batch_rows = lay.m * blocks_per_batch
-        # sum_col_vec halves by baby-step/giant-step hoisted groups (log_baby > 0)
-        self.log_baby = (self.log_g + 1) // 2 if (bsgs and self.log_g > 0) else 0
+        # sum_col_vec halves and sum_rows as grouped hoisted rotate-and-sums
+        # (groups of at most log_baby / log_baby_rows bits; 0 = one key switch
+        # per power-of-two rotation)
+        if not bsgs:
+            self.log_baby = self.log_baby_rows = 0
+        else:
+            self.log_baby = (self.log_g + 1) // 2 if bsgs_bits is None else bsgs_bits
+            self.log_baby_rows = (self.log_m + 1) // 2 if rows_bits is None else rows_bits
+            if not (0 <= self.log_baby <= 5 and 0 <= self.log_baby_rows <= 5):
+                raise ValueError("hoisted groups hold at most 31 rotations: group bits must be in [0, 5]")
+            if self.log_g == 0:
+                self.log_baby = 0
+            if self.log_m == 0:
+                self.log_baby_rows = 0
         self.qpoly = poly.complement().padded(3)
         self.lib = _lib.load()
         _bind(self.lib)
@@ -254,13 +285,16 @@ class FusedTrainer:
         # keys: left/right 2^i (sum_col_vec), g*2^i (sum_rows)
         S = ck.slots
         if self.log_baby > 0:
-            bs, gs = self.log_baby, self.log_g - self.log_baby
-            steps = list(range(1, 1 << bs)) + [k << bs for k in range(1, 1 << gs)]
+            steps = [k for grp in grouped_steps(self.log_g, self.log_baby) for k in grp]
         else:
             steps = [1 << i for i in range(self.log_g)]
+        if self.log_baby_rows > 0:
+            rsteps = [k for grp in grouped_steps(self.log_m, self.log_baby_rows, lay.g) for k in grp]
+        else:
+            rsteps = [lay.g << i for i in range(self.log_m)]
         self.gal_left = [pow(5, k, 2 * N) for k in steps]
         self.gal_right = [pow(5, S - k, 2 * N) for k in steps]
-        self.gal_rows = [pow(5, lay.g << i, 2 * N) for i in range(self.log_m)]
+        self.gal_rows = [pow(5, k % S, 2 * N) for k in rsteps]
         keys = lambda gs: (ctypes.c_void_p * max(1, len(gs)))(*[ctx.galois_key(g).data_ptr() for g in gs])
         self._k_left, self._k_right, self._k_rows = keys(self.gal_left), keys(self.gal_right), keys(self.gal_rows)
         self._masks: dict = {}
@@ -362,7 +396,7 @@ class FusedTrainer:
                        lw=plan.lw, rlk=self.ctx.rlk.data_ptr(), rot_left=self._k_left, rot_right=self._k_right,
                        rot_rows=self._k_rows, mask_pt=self._mask(plan.lw, plan.mask_scale).data_ptr(),
                        consts=self.consts_dev.data_ptr(), grad=self.grad.data_ptr(), phase=phase,
-                       log_baby=self.log_baby)
+                       log_baby=self.log_baby, log_baby_rows=self.log_baby_rows)
 
     def _upload_consts(self, plan: IterPlan):
         i = self._ci

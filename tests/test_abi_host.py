@@ -86,3 +86,21 @@ def test_encoder_constant_is_constant_polynomial():
     enc = Encoder(8)
     c = enc.encode(np.full(enc.slots, 0.75), 2.0 ** 30)
     assert c[0] == round(0.75 * 2 ** 30) and np.all(np.abs(c[1:]) <= 1)
+
+
+def test_rotsum_groups_host_rule_matches_library():
+    """helr_rotsum_groups (csrc/nag.cu) and the driver's / oracle's grouping
+    rule agree; it is a host-only entry point, callable without a GPU."""
+    import ctypes
+    from oracle import schedule as osched
+    from paper_2406_13221_b200 import _lib
+    from paper_2406_13221_b200.driver import rotsum_groups
+    lib = _lib.load()
+    bits = (ctypes.c_int * 64)()
+    for total in range(0, 17):
+        for mx in range(0, 9):
+            ng = lib.helr_rotsum_groups(total, mx, bits)
+            want = rotsum_groups(total, mx)
+            assert list(bits[:ng]) == want == osched.rotsum_groups(total, mx)
+            if want:
+                assert sum(want) == total and max(want) <= mx

@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 
 from paper_2406_13221_b200 import _lib
 from paper_2406_13221_b200.ckks import GpuContext
-from paper_2406_13221_b200.driver import NagArgs, _bind, plan_iteration, row_mask
+from paper_2406_13221_b200.driver import NagArgs, _bind, grouped_steps, plan_iteration, row_mask
 from paper_2406_13221_b200.optimizer import BASELINE_CUBIC
 from paper_2406_13221_b200.params import CkksParams
 from oracle.oracle import Oracle
@@ -30,6 +30,9 @@ CASES = {
     "toy_shape": (13, 8, 3, 1, 1, 5),
     "n4096_r3_c1_L9": (12, 9, 3, 3, 1, 6),
 }
+
+
+GROUPINGS = {"chain": None, "bsgs": "half", "radix2": 2}
 
 
 def _setup(case, seed=11, bsgs=False):
@@ -52,21 +55,32 @@ def _setup(case, seed=11, bsgs=False):
     ctx.encrypt_to(ctx.encoder.encode(bvals, s_top), bbar, top)
     qpoly = BASELINE_CUBIC.complement().padded(3)
     plan = plan_iteration(P, top, s_top, s_top, s_top, s_top, qpoly, 1.05, 0.37)
-    log_baby = (log_g + 1) // 2 if bsgs else 0
+    mode = GROUPINGS[bsgs] if isinstance(bsgs, str) else ("half" if bsgs else None)
+    if mode is None:
+        log_baby = log_baby_rows = 0
+    elif mode == "half":
+        log_baby, log_baby_rows = (log_g + 1) // 2, (log_m + 1) // 2
+    else:
+        log_baby = log_baby_rows = mode
     if log_baby:
-        steps = list(range(1, 1 << log_baby)) + [k << log_baby for k in range(1, 1 << (log_g - log_baby))]
+        steps = [k for grp in grouped_steps(log_g, log_baby) for k in grp]
     else:
         steps = [1 << i for i in range(log_g)]
+    if log_baby_rows:
+        rsteps = [k for grp in grouped_steps(log_m, log_baby_rows, 1 << log_g) for k in grp]
+    else:
+        rsteps = [(1 << log_g) << i for i in range(log_m)]
     gl = [pow(5, k, 2 * n) for k in steps]
     gr = [pow(5, S - k, 2 * n) for k in steps]
-    gw = [pow(5, (1 << log_g) << i, 2 * n) for i in range(log_m)]
+    gw = [pow(5, k % S, 2 * n) for k in rsteps]
     arr = lambda gs: (ctypes.c_void_p * max(1, len(gs)))(*[ctx.galois_key(g).data_ptr() for g in gs])
     mask = ctx._plain(ctx.encoder.encode(row_mask(S, 1 << log_g), plan.mask_scale), top - 1)
     consts = torch.from_numpy(plan.consts.view(np.int64)).to(ctx.device)
     grad = ctx._empty((C, 2, L, n))
     keys = (arr(gl), arr(gr), arr(gw))
     return dict(P=P, ctx=ctx, z=z, wv=wv, bbar=bbar, plan=plan, mask=mask, consts=consts, grad=grad, keys=keys,
-                R=R, C=C, log_g=log_g, log_m=log_m, gals=gl + gr + gw, vals=(zvals, wv_vals, bvals), log_baby=log_baby)
+                R=R, C=C, log_g=log_g, log_m=log_m, gals=gl + gr + gw, vals=(zvals, wv_vals, bvals), log_baby=log_baby,
+                log_baby_rows=log_baby_rows)
 
 
 def _args(d, z_ptr, phase):
@@ -76,7 +90,7 @@ def _args(d, z_ptr, phase):
                    v=d["wv"].data_ptr() + C * cs, bbar=d["bbar"].data_ptr(), lw=d["P"].top_level,
                    rlk=ctx.rlk.data_ptr(), rot_left=d["keys"][0], rot_right=d["keys"][1], rot_rows=d["keys"][2],
                    mask_pt=d["mask"].data_ptr(), consts=d["consts"].data_ptr(), grad=d["grad"].data_ptr(),
-                   phase=phase, log_baby=d["log_baby"])
+                   phase=phase, log_baby=d["log_baby"], log_baby_rows=d["log_baby_rows"])
 
 
 def _oracle_inputs(d):
@@ -86,7 +100,7 @@ def _oracle_inputs(d):
     return orc, gkeys, u64(ctx.rlk), u64(d["mask"]), d["plan"].consts
 
 
-@pytest.mark.parametrize("bsgs", [False, True])
+@pytest.mark.parametrize("bsgs", list(GROUPINGS))
 @pytest.mark.parametrize("case", list(CASES))
 def test_fused_iteration_matches_oracle(case, bsgs):
     d = _setup(case, bsgs=bsgs)
@@ -100,15 +114,16 @@ def test_fused_iteration_matches_oracle(case, bsgs):
     orc, gkeys, rlk, mask, consts = _oracle_inputs(d)
     lw = d["P"].top_level
     w2, v2 = osched.nag_iteration(orc, z_np, w_np, v_np, b_np, lw, rlk, gkeys, mask, consts, d["log_g"], d["log_m"],
-                                  log_baby=d["log_baby"])
+                                  log_baby=d["log_baby"], log_baby_rows=d["log_baby_rows"])
     out = u64(d["wv"])
     lo = lw - 7 + 1
     np.testing.assert_array_equal(out[:C, :, :lo], w2[:, :, :lo])
     np.testing.assert_array_equal(out[C:, :, :lo], v2[:, :, :lo])
 
 
-def test_fused_full_batch_phases_match_oracle():
-    d = _setup("n1024_r2_c2", seed=3)
+@pytest.mark.parametrize("bsgs", ["chain", "bsgs"])
+def test_fused_full_batch_phases_match_oracle(bsgs):
+    d = _setup("n1024_r2_c2", seed=3, bsgs=bsgs)
     ctx, C, R = d["ctx"], d["C"], d["R"]
     lib = _lib.load()
     _bind(lib)
@@ -124,20 +139,22 @@ def test_fused_full_batch_phases_match_oracle():
         args = _args(d, zz.data_ptr(), 1 if k == 0 else 2)
         _lib.check(lib.helr_nag_iteration(ctx.handle, ctypes.byref(args), stream), "nag phase")
         grad_ref = osched.nag_iteration(orc, u64(zz), w_np, v_np, b_np, lw, rlk, gkeys, mask, consts, d["log_g"],
-                                        d["log_m"], phase=1 if k == 0 else 2, grad=grad_ref)
+                                        d["log_m"], phase=1 if k == 0 else 2, grad=grad_ref, log_baby=d["log_baby"],
+                                        log_baby_rows=d["log_baby_rows"])
     lo = lw - 5 + 1
     np.testing.assert_array_equal(u64(d["grad"])[:, :, :lo], grad_ref[:, :, :lo])
     args = _args(d, d["z"].data_ptr(), 3)
     _lib.check(lib.helr_nag_iteration(ctx.handle, ctypes.byref(args), stream), "nag finish")
     w2, v2 = osched.nag_iteration(orc, None if False else u64(d["z"]), w_np, v_np, b_np, lw, rlk, gkeys, mask, consts,
-                                  d["log_g"], d["log_m"], phase=3, grad=grad_ref)
+                                  d["log_g"], d["log_m"], phase=3, grad=grad_ref, log_baby=d["log_baby"],
+                                  log_baby_rows=d["log_baby_rows"])
     out = u64(d["wv"])
     lo = lw - 7 + 1
     np.testing.assert_array_equal(out[:C, :, :lo], w2[:, :, :lo])
     np.testing.assert_array_equal(out[C:, :, :lo], v2[:, :, :lo])
 
 
-@pytest.mark.parametrize("bsgs", [False, True])
+@pytest.mark.parametrize("bsgs", list(GROUPINGS))
 def test_fused_iteration_values(bsgs):
     """Decrypted W', V' equal the plaintext update within CKKS noise."""
     d = _setup("toy_shape", seed=5, bsgs=bsgs)

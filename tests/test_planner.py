@@ -20,7 +20,7 @@ def _gal(k, n):
     return pow(5, k % (n // 2), 2 * n)
 
 
-@pytest.mark.parametrize("bsgs", [0, 2])
+@pytest.mark.parametrize("bsgs", [0, 2, 3])
 @pytest.mark.parametrize("R,C", [(1, 1), (2, 2)])
 def test_planned_iteration_matches_plaintext(R, C, bsgs):
     log_n, L = 10, 8
@@ -48,14 +48,17 @@ def test_planned_iteration_matches_plaintext(R, C, bsgs):
     mult, eta = 1.02, -0.6
     plan = plan_iteration(P, top, s_top, s_top, s_top, s_b, qp, mult, eta)
     if bsgs:
-        steps = list(range(1, 1 << bsgs)) + [k << bsgs for k in range(1, 1 << (log_g - bsgs))]
+        steps = [k for grp in osched.grouped_steps(log_g, bsgs) for k in grp]
+        rsteps = [k for grp in osched.grouped_steps(log_m, bsgs, g) for k in grp]
     else:
         steps = [1 << i for i in range(log_g)]
-    gals = [_gal(k, N) for k in steps] + [_gal(-k, N) for k in steps] + [_gal(g << i, N) for i in range(log_m)]
+        rsteps = [g << i for i in range(log_m)]
+    gals = [_gal(k, N) for k in steps] + [_gal(-k, N) for k in steps] + [_gal(k, N) for k in rsteps]
     gk = {x: orc.keygen_switch(sk, x, 3, x) for x in set(gals)}
     rlk = orc.keygen_switch(sk, 0, 3, 0)
     mask = orc.encode_plain(enc.encode(row_mask(S, g), plan.mask_scale), top - 1)[0]
-    w2, v2 = osched.nag_iteration(orc, z, w, v, bb, top, rlk, gk, mask, plan.consts, log_g, log_m, log_baby=bsgs)
+    w2, v2 = osched.nag_iteration(orc, z, w, v, bb, top, rlk, gk, mask, plan.consts, log_g, log_m, log_baby=bsgs,
+                                  log_baby_rows=bsgs)
     got_w = enc.decode(orc.decrypt(sk, w2, 0), plan.s_out).real
     got_v = enc.decode(orc.decrypt(sk, v2, 0), plan.s_out).real
     # plaintext model
