@@ -42,10 +42,10 @@ CATS = ["ntt", "modup", "ks_inner", "moddown", "tensor", "rescale", "elementwise
 
 WORKLOADS = {
     # name: (dataset factory kwargs, log_n, L primes, dnum, rows per block, blocks per batch, mode)
-    "paper_mini": dict(data="paper", log_n=16, L=8, dnum=3, rows=128, blocks=8, mode="mini_batch"),
-    "paper_full": dict(data="paper", log_n=16, L=8, dnum=3, rows=128, blocks=8, mode="full_batch"),
-    "medium": dict(data="medium", log_n=15, L=8, dnum=3, rows=1024, blocks=1, mode="mini_batch"),
-    "toy": dict(data="toy", log_n=13, L=8, dnum=3, rows=128, blocks=1, mode="mini_batch"),
+    "paper_mini": dict(data="paper", log_n=16, L=8, dnum=2, rows=128, blocks=8, mode="mini_batch"),
+    "paper_full": dict(data="paper", log_n=16, L=8, dnum=2, rows=128, blocks=8, mode="full_batch"),
+    "medium": dict(data="medium", log_n=15, L=8, dnum=2, rows=1024, blocks=1, mode="mini_batch"),
+    "toy": dict(data="toy", log_n=13, L=8, dnum=2, rows=128, blocks=1, mode="mini_batch"),
 }
 
 

@@ -108,8 +108,10 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
     if (max_batch < 1) max_batch = 1;
     const int n = 1 << log_n;
     for (int i = 0; i < L + K; i++) {
-        if (primes[i] >= (1ull << 62) || (primes[i] - 1) % (2ull * n) != 0) {
-            set_error("primes must be < 2^62 and = 1 mod 2N");
+        // < 2^61: lazy NTT values in [0, 8q) and 128-bit key-product sums of
+        // up to 63 terms must fit their words
+        if (primes[i] >= (1ull << 61) || (primes[i] - 1) % (2ull * n) != 0) {
+            set_error("primes must be < 2^61 and = 1 mod 2N");
             return HELR_EINVAL;
         }
         if (hpow(psi[i], (u64)n, primes[i]) != primes[i] - 1) {

@@ -21,6 +21,16 @@ DV u64 shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) {
     u64 h = mulhi64(a, wsh);
     return a * w - h * q;
 }
+// Shoup with an approximate quotient: the high word of a * wsh without the
+// low x low partial product and the low halves of the cross products (one
+// 32x32->64 and two 32x32->hi32 multiplies instead of four 32x32->64).  The
+// quotient is at most 2 below Shoup's, so the result is in [0, 4q) for any
+// a < 2^64 — the NTT keeps lazy values in [0, 8q) (all primes < 2^61).
+DV u64 shoup_lazy4(u64 a, u64 w, u64 wsh, u64 q) {
+    const u32 a0 = (u32)a, a1 = (u32)(a >> 32), w0 = (u32)wsh, w1 = (u32)(wsh >> 32);
+    const u64 h = (u64)a1 * w1 + (u64)__umulhi(a1, w0) + (u64)__umulhi(a0, w1);
+    return a * w - h * q;
+}
 DV u64 csub(u64 a, u64 q) { return a >= q ? a - q : a; }
 DV u64 shoup(u64 a, u64 w, u64 wsh, u64 q) { return csub(shoup_lazy(a, w, wsh, q), q); }
 

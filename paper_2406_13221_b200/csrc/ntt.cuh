@@ -1,9 +1,13 @@
 // ntt.cuh — negacyclic NTT passes for sm_100a.
 //
 // Forward: Cooley-Tukey over bit-reversed powers of psi with Harvey lazy
-// butterflies (values in [0, 4q)); output slot i = a(psi^(2 brv(i) + 1)).
-// Inverse: Gentleman-Sande with psi^-1, lazy in [0, 2q), N^-1 folded into
-// the last stage.  Both equal, residue for residue, the oracle's loops.
+// butterflies; output slot i = a(psi^(2 brv(i) + 1)).  Inverse:
+// Gentleman-Sande with psi^-1, N^-1 folded into the last stage.  Twiddle
+// products use Shoup with an approximate quotient (shoup_lazy4, result in
+// [0, 4q)), so lazy values live in [0, 8q) forward and [0, 4q) inverse —
+// 8q < 2^64 because every prime is below 2^61 (checked at context
+// creation).  Outputs are reduced to [0, q), so both transforms equal,
+// residue for residue, the oracle's loops.
 //
 // Decomposition.  log N = s1 + s2.  The first s1 forward stages only mix
 // elements with equal index mod 2^s2 ("columns", stride 2^s2); the last s2
@@ -55,6 +59,7 @@ struct has_vec<F, decltype((void)F::kVec)> { static constexpr bool value = F::kV
 // One radix-2 stage on a thread's R registers: pairs (i, i + 2^H), the
 // twiddle shared by every pair with the same i >> (H + 1).  H is a template
 // parameter so every register index is static (no local-memory arrays).
+// q2 below is the lazy half-range 4q: forward inputs/outputs in [0, 8q).
 template <int R, int H>
 __device__ __forceinline__ void fwd_stage(u64 (&x)[R], const ulonglong2* __restrict__ W2, int tb0, u64 q, u64 q2) {
 #pragma unroll
@@ -65,7 +70,7 @@ __device__ __forceinline__ void fwd_stage(u64 (&x)[R], const ulonglong2* __restr
             const int i = (j << (H + 1)) + t;
             u64 u = x[i];
             u = u >= q2 ? u - q2 : u;
-            const u64 v = shoup_lazy(x[i + (1 << H)], w.x, w.y, q);
+            const u64 v = shoup_lazy4(x[i + (1 << H)], w.x, w.y, q);
             x[i] = u + v;
             x[i + (1 << H)] = u + q2 - v;
         }
@@ -82,7 +87,7 @@ __device__ __forceinline__ void inv_stage(u64 (&x)[R], const ulonglong2* __restr
             const u64 u = x[i], v = x[i + (1 << H)];
             const u64 sum = u + v;
             x[i] = sum >= q2 ? sum - q2 : sum;
-            x[i + (1 << H)] = shoup_lazy(u + q2 - v, w.x, w.y, q);
+            x[i + (1 << H)] = shoup_lazy4(u + q2 - v, w.x, w.y, q);
         }
     }
 }
@@ -93,8 +98,8 @@ __device__ __forceinline__ void inv_last_stage(u64 (&x)[R], u64 ni, u64 nis, u64
     for (int i = 0; i < R; i++) {
         if (i & (1 << H)) continue;
         const u64 u = x[i], v = x[i + (1 << H)];
-        x[i] = shoup_lazy(u + v, ni, nis, q);
-        x[i + (1 << H)] = shoup_lazy(u + q2 - v, wl, wls, q);
+        x[i] = shoup_lazy4(u + v, ni, nis, q);
+        x[i + (1 << H)] = shoup_lazy4(u + q2 - v, wl, wls, q);
     }
 }
 template <int R>
@@ -138,7 +143,7 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     const int z = blockIdx.z;
     const int prime = map.prime[li];
     const u64 q = tb.q[prime];
-    const u64 q2 = 2 * q;
+    const u64 q2 = 4 * q;  // lazy half-range (see fwd_stage)
     const int n = 1 << a.log_n;
     const int s2 = a.log_n - LOG_T;  // used by column passes
     const ulonglong2* W2 = reinterpret_cast<const ulonglong2*>(INV ? tb.itw : tb.tw) + (size_t)prime * n;
@@ -212,9 +217,10 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
         if (g == NG - 1) {
 #pragma unroll
             for (int i = 0; i < R; i++) {
-                if (a.final_out) {
+                if (a.final_out) {  // forward [0, 8q), inverse [0, 4q) -> [0, q)
                     u64 v = x[i];
                     if (!INV) v = v >= q2 ? v - q2 : v;
+                    v = v >= 2 * q ? v - 2 * q : v;
                     x[i] = v >= q ? v - q : v;
                 }
             }
@@ -271,6 +277,11 @@ struct StBuf {
 // The first pass reads through `ld`, the last pass writes through `st`; with
 // two passes the intermediate goes through `mid` (item stride mid_stride,
 // limb offsets from map) which may alias the storer's buffer.
+// Launches of fewer than NTT_SMALL_GRID full-size CTAs (single-ciphertext
+// key switches at low levels) use CTAs a quarter the size, so four times as
+// many SMs share the latency-bound work.
+constexpr long long NTT_SMALL_GRID = 2 * 148;
+
 template <int LOG_T, bool IS_COL, bool INV, class Ld, class St>
 static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
                             int log_n, int st0, int final_out, int count, cudaStream_t s) {
@@ -279,16 +290,23 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
     // column passes: 16 adjacent columns (128-byte rows); row passes: ~4096 elements per CTA
     constexpr int COLS_ROW = (4096 / T) > 0 ? (4096 / T) : 1;
     constexpr int COLS = IS_COL ? 16 : COLS_ROW;
+    constexpr int COLS_S = COLS >= 4 ? COLS / 4 : 1;
     const int subs = IS_COL ? (1 << (log_n - LOG_T)) : (1 << (log_n - LOG_T));
     const int cols = subs < COLS ? subs : COLS;  // tiny rings: fewer sub-transforms than COLS
     NttPassArgs a{log_n, st0, final_out};
-    dim3 grid(subs / cols, map.count, count);
-    const int threads = T * cols / (1 << LOG_R);
     count_launches(1);
     if (cols == COLS) {
-        ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV><<<grid, threads, 0, s>>>(ld, st, tb, map, a);
+        const long long full = (long long)(subs / COLS) * map.count * count;
+        if (COLS_S < COLS && full < NTT_SMALL_GRID && log_n >= 12) {
+            dim3 grid(subs / COLS_S, map.count, count);
+            ntt_pass<LOG_T, LOG_R, COLS_S, IS_COL, INV><<<grid, T * COLS_S / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
+            return;
+        }
+        dim3 grid(subs / COLS, map.count, count);
+        ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV><<<grid, T * COLS / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
     } else {
         // only reachable for single-pass rings (subs == 1)
+        dim3 grid(subs / cols, map.count, count);
         ntt_pass<LOG_T, LOG_R, 1, IS_COL, INV><<<grid, T / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
     }
 }

@@ -11,8 +11,8 @@ chain q_0 (about 2**60) and q_1..q_{L-1} (about 2**log_scale, alternately
 just above and below so the per-level scale stays close to 2**log_scale),
 K special primes p_k (about 2**61) for hybrid key switching with ``dnum``
 digits of ``alpha`` limbs, and one primitive 2N-th root of unity per prime.
-All primes are below 2**62 so the lazy [0, 4q) NTT butterflies never
-overflow a 64-bit word.  Everything here is plain integer arithmetic and
+All primes are below 2**61 so the lazy [0, 8q) NTT butterflies (approximate
+Shoup quotients) and the 128-bit key-product accumulators never overflow.  Everything here is plain integer arithmetic and
 deterministic, so the device library and the CPU oracle are handed the
 identical chain and roots.
 
@@ -204,8 +204,8 @@ class CkksParams:
             raise ValueError(f"need alpha = {self.alpha} special primes, got {len(self.p)}")
         m = 2 << self.log_n
         for x in tuple(self.q) + tuple(self.p):
-            if x >= (1 << 62) or (x - 1) % m or not is_prime(x):
-                raise ValueError(f"{x} is not an NTT-friendly prime < 2**62 for N=2**{self.log_n}")
+            if x >= (1 << 61) or (x - 1) % m or not is_prime(x):
+                raise ValueError(f"{x} is not an NTT-friendly prime < 2**61 for N=2**{self.log_n}")
         if len(set(self.q) | set(self.p)) != len(self.q) + len(self.p):
             raise ValueError("primes must be distinct")
         if not 0 < self.cbd_eta <= 32:

@@ -22,9 +22,9 @@ GOLD = Path(__file__).resolve().parent / "golden"
 TOL = 1e-6
 
 
-def _run(name, ds, log_n, rows, blocks, mode, n_iters, use_graph=False):
+def _run(name, ds, log_n, rows, blocks, mode, n_iters, use_graph=False, dnum=2):
     gold = np.load(GOLD / f"{name}.npz")
-    ck = CkksParams.generate(log_n=log_n, n_q=8, dnum=3)
+    ck = CkksParams.generate(log_n=log_n, n_q=8, dnum=dnum)
     ctx = GpuContext(ck, seed=2, max_batch=8)
     tr = FusedTrainer(ctx, ds, rows_per_block=rows, blocks_per_batch=blocks, mode=mode, use_graph=use_graph)
     its = list(gold["iterations"])
@@ -47,7 +47,7 @@ def test_toy_all_iterations():
 
 
 def test_toy_with_cuda_graph():
-    w, a = _run("toy", data.toy_dataset(), 13, 128, 1, "mini_batch", 24, use_graph=True)
+    w, a = _run("toy", data.toy_dataset(), 13, 128, 1, "mini_batch", 24, use_graph=True, dnum=3)
     assert w < TOL and a < TOL
 
 

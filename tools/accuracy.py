@@ -25,11 +25,11 @@ CFG = {
 }
 
 
-def run(name, refresh_bits=None):
+def run(name, refresh_bits=None, dnum=2):
     make, log_n, rows, blocks, mode = CFG[name]
     gold = np.load(ROOT / "tests" / "golden" / f"{name}.npz")
     ds = make()
-    ctx = GpuContext(CkksParams.generate(log_n=log_n, n_q=8, dnum=3), seed=2, max_batch=8)
+    ctx = GpuContext(CkksParams.generate(log_n=log_n, n_q=8, dnum=dnum), seed=2, max_batch=8)
     kw = {} if refresh_bits is None else dict(refresh_bits=refresh_bits)
     tr = FusedTrainer(ctx, ds, rows_per_block=rows, blocks_per_batch=blocks, mode=mode, use_graph=True, **kw)
     refresh_bits = tr.refresh_bits
@@ -46,7 +46,7 @@ def run(name, refresh_bits=None):
             da = abs(auroc(ds.y, ds.X @ w) - float(gold["auc"][k]))
             worst_w, worst_a = max(worst_w, dw), max(worst_a, da)
             curve.append((t, dw, da))
-    out = dict(workload=name, refresh_bits=refresh_bits, iterations=its[-1], max_abs_dw=worst_w, max_abs_dauc=worst_a,
+    out = dict(workload=name, refresh_bits=refresh_bits, dnum=dnum, iterations=its[-1], max_abs_dw=worst_w, max_abs_dauc=worst_a,
                final_auc=float(gold["auc"][-1]), seconds=time.time() - t0,
                curve=curve if len(curve) < 400 else [c for c in curve if c[0] % 16 == 0])
     print(json.dumps(out), flush=True)
@@ -54,6 +54,9 @@ def run(name, refresh_bits=None):
 
 
 if __name__ == "__main__":
+    # spec: name[:refresh_bits[:dnum]]
     for spec in sys.argv[1:] or ["toy", "medium", "paper_mini"]:
-        name, _, bits = spec.partition(":")
-        run(name, int(bits) if bits else None)
+        parts = spec.split(":")
+        bits = int(parts[1]) if len(parts) > 1 and parts[1] else None
+        dn = int(parts[2]) if len(parts) > 2 else 2
+        run(parts[0], bits, dn)

@@ -36,6 +36,18 @@ __global__ void k(uint64_t* out, uint32_t seed) {
             if (OP == 4) asm volatile("mul.hi.u64 %0, %0, %1;" : "+l"(w[c]) : "l"(m64));
             if (OP == 5) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[c]) : "d"(0.999999));
             if (OP == 6) asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+f"(f[c]) : "f"(0.999f));
+            if (OP == 7) {  // u64 -> f64 -> u64 round trip (I2F.F64.U64 + F2I.U64.F64)
+                double t;
+                asm volatile("cvt.rn.f64.u64 %0, %1;" : "=d"(t) : "l"(w[c]));
+                asm volatile("cvt.rzi.u64.f64 %0, %1;" : "=l"(w[c]) : "d"(t));
+            }
+            if (OP == 8) asm volatile("cvt.rmi.f64.f64 %0, %0;" : "+d"(d[c]));  // floor
+            if (OP == 9) asm volatile("mul.rn.f64 %0, %0, %1;" : "+d"(d[c]) : "d"(1.0000001));
+            if (OP == 10) {  // 32-bit -> f64 (I2F.F64.U32)
+                double t;
+                asm volatile("cvt.rn.f64.u32 %0, %1;" : "=d"(t) : "r"(a[c]));
+                d[c] += t;
+            }
         }
     }
     uint64_t s = 0;
@@ -78,5 +90,9 @@ int main() {
     run<4>("mul.hi.u64", p.multiProcessorCount, clk);
     run<5>("DFMA", p.multiProcessorCount, clk);
     run<6>("FFMA", p.multiProcessorCount, clk);
+    run<7>("cvt u64>f64>u64", p.multiProcessorCount, clk);
+    run<8>("floor f64", p.multiProcessorCount, clk);
+    run<9>("DMUL", p.multiProcessorCount, clk);
+    run<10>("cvt u32>f64 +DADD", p.multiProcessorCount, clk);
     return 0;
 }
