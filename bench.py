@@ -13,7 +13,7 @@ update, and the refresh stand-in of W/V (every iteration at L = 8 primes).
 
 Timing: CUDA events on the launching stream, barrier + synchronize on both
 sides, max over ranks; every step reads a different batch (64 MiB of
-ciphertexts) and streams 24 Galois keys (~830 MB), far beyond the 126 MB L2,
+ciphertexts) and streams ~80 Galois keys (~2 GB), far beyond the 126 MB L2,
 so no flush is needed between steps.  Multi-GPU: independent replicas
 (the mini-batch path does not shard), scaling "weak".
 """
@@ -347,7 +347,7 @@ def main():
                        "K": ck.K, "dnum": ck.dnum, "batch_rows": tr.batch_rows, "cts_per_batch": tr.rows,
                        "batches": tr.n_batches, "mode": wl["mode"], "parallelism": "replicas",
                        "cuda_graph": tr.use_graph, "rotsum_group_bits": tr.log_baby, "rows_group_bits": tr.log_baby_rows,
-                       "l2": "no flush needed: each step streams a new 64 MiB batch and ~830 MB of keys"},
+                       "l2": "no flush needed: each step streams a new 64 MiB batch and ~2 GB of keys"},
             "epoch_s": tr.n_batches / (value / ws),
             "hbm_gbs_step": step_gb / (ms / steps / 1000.0),
             "algorithmic_gb_per_step": step_gb,

@@ -55,6 +55,13 @@ template <class F, class = void>
 struct has_vec { static constexpr bool value = false; };
 template <class F>
 struct has_vec<F, decltype((void)F::kVec)> { static constexpr bool value = F::kVec; };
+// kTile: the last row pass stages its outputs through shared memory and calls
+// store2 on coalesced consecutive pairs (storers that read other global
+// arrays at the output position, e.g. StCombine)
+template <class F, class = void>
+struct has_tile { static constexpr bool value = false; };
+template <class F>
+struct has_tile<F, decltype((void)F::kTile)> { static constexpr bool value = F::kTile; };
 
 // One radix-2 stage on a thread's R registers: pairs (i, i + 2^H), the
 // twiddle shared by every pair with the same i >> (H + 1).  H is a template
@@ -224,7 +231,20 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
                     x[i] = v >= q ? v - q : v;
                 }
             }
-            if constexpr (!IS_COL && has_vec<St>::value) {
+            if constexpr (!IS_COL && has_tile<St>::value) {
+                if (NG > 1) __syncthreads();  // this group's shared-memory reads are done
+#pragma unroll
+                for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = x[i];
+                __syncthreads();
+                constexpr int TOT = T * COLS;
+                const int nthr = T * COLS / R;
+#pragma unroll 4
+                for (int e = 2 * tid; e < TOT; e += 2 * nthr) {
+                    const int c2 = e >> LOG_T, k = e & (T - 1);
+                    const u64 v0 = sm[c2 * SROW + k + (k >> 4)], v1 = sm[c2 * SROW + k + 1 + ((k + 1) >> 4)];
+                    st.store2(z, li, prime, ((blockIdx.x * COLS + c2) << LOG_T) + k, make_ulonglong2(v0, v1));
+                }
+            } else if constexpr (!IS_COL && has_vec<St>::value) {
                 if (lo == 0) {
 #pragma unroll
                     for (int i = 0; i < R; i += 2) st.store2(z, li, prime, goff(base + i), make_ulonglong2(x[i], x[i + 1]));
@@ -245,6 +265,9 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
 }
 
 // ---- plain functors: strided limb buffers -------------------------------
+#ifndef HELR_STBUF_TILE
+#define HELR_STBUF_TILE false
+#endif
 struct LdBuf {
     static constexpr bool kVec = true;
     const u64* base;
@@ -260,6 +283,7 @@ struct LdBuf {
 };
 struct StBuf {
     static constexpr bool kVec = true;
+    static constexpr bool kTile = HELR_STBUF_TILE;
     u64* base;
     long long item_stride;
     LimbMap map;

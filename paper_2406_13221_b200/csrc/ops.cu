@@ -38,6 +38,8 @@ static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 static inline int blocks_for(long long n, int t) { return (int)((n + t - 1) / t); }
 
 __device__ __forceinline__ int brv_dev(int x, int log_n) { return (int)(__brev((unsigned)x) >> (32 - log_n)); }
+__device__ __forceinline__ ulonglong2 ld2(const u64* p) { return *reinterpret_cast<const ulonglong2*>(p); }
+__device__ __forceinline__ void st2(u64* p, u64 x, u64 y) { *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(x, y); }
 // NTT-slot permutation of X -> X^g: out[i] = in[perm(i)]
 __device__ __forceinline__ int galois_perm(int i, u64 g, int log_n) {
     const u64 two_n = 2ull << log_n;
@@ -406,6 +408,7 @@ extern "C" int helr_refresh(helr_ctx* c, const uint64_t* sk, const uint64_t* a, 
 
 // ---------------------------------------------------------------------------
 // rescale: out_i = (x_i - NTT_i([INTT_l(x_l)]_centred mod q_i)) * q_l^-1
+// (the combine runs in the storer of the last NTT pass, StCombine)
 __global__ void k_rescale_conv(const u64* r, u64* t, int n, int l, Tables tb) {
     // r: [items][N] coefficient form mod q_l;  t: [items][l][N]
     const int it = blockIdx.y;
@@ -419,19 +422,6 @@ __global__ void k_rescale_conv(const u64* r, u64* t, int n, int l, Tables tb) {
         }
     }
 }
-__global__ void k_rescale_final(const u64* x, long long xs, const u64* t, u64* out, long long os, int n, int L, int l,
-                                const u64* qlinv, const u64* qlinv_sh, Tables tb) {
-    const int it = blockIdx.z, p = blockIdx.y;  // it = item*2 + poly
-    const int item = it >> 1, poly = it & 1;
-    const u64 q = tb.q[p];
-    const u64 w = qlinv[(size_t)l * L + p], wsh = qlinv_sh[(size_t)l * L + p];
-    const u64* xp = x + (size_t)item * xs + ((size_t)poly * L + p) * n;
-    const u64* tp = t + ((size_t)it * l + p) * n;
-    u64* op = out + (size_t)item * os + ((size_t)poly * L + p) * n;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        op[i] = shoup(sub_mod(xp[i], tp[i], q), w, wsh, q);
-}
-
 // polynomial (item, poly) of a strided ciphertext batch, limb `li` offset added by the caller
 struct LdPolyLimb {
     const u64* base;   // points at limb l of poly 0 of item 0
@@ -440,6 +430,73 @@ struct LdPolyLimb {
         return base[(size_t)(z >> 1) * item_stride + (size_t)(z & 1) * poly_stride + off];
     }
 };
+
+// Last-NTT-pass storer that finishes a ModDown / rescale in place of a
+// separate combine kernel: out = (x - v) * w_p mod q [+ add_a] [+ sum_t
+// sigma_t(add_p) on poly 0], v being the NTT output.  Index decoding:
+// per_poly > 0: item = z, li = poly * per_poly + p;  per_poly == 0:
+// item = z >> 1, poly = z & 1, p = li.
+struct StCombine {
+    static constexpr bool kVec = true;
+    static constexpr bool kTile = true;
+    u64* out;
+    long long out_is, out_ps;
+    const u64* x;
+    long long x_is, x_ps;
+    const u64* w;
+    const u64* wsh;
+    const u64* q;
+    const u64* add_a;
+    long long a_is, a_ps;
+    const u64* add_p;
+    long long p_is;
+    int ngal, log_n, n, per_poly;
+    long long gal[HELR_MAX_HOIST];
+    __device__ __forceinline__ void decode(int z, int li, int& item, int& poly, int& p) const {
+        if (per_poly > 0) { item = z; poly = li >= per_poly ? 1 : 0; p = li - poly * per_poly; }
+        else { item = z >> 1; poly = z & 1; p = li; }
+    }
+    __device__ __forceinline__ u64 addends(u64 r, int item, int poly, int p, int off, u64 qq, u64 av) const {
+        if (add_a) r = add_mod(r, av, qq);
+        if (add_p && poly == 0) {
+            const u64* pp = add_p + (size_t)item * p_is + (size_t)p * n;
+            for (int t = 0; t < ngal; t++) r = add_mod(r, pp[galois_perm(off, (u64)gal[t], log_n)], qq);
+        }
+        return r;
+    }
+    __device__ __forceinline__ void operator()(int z, int li, int, int off, u64 v) const {
+        int item, poly, p;
+        decode(z, li, item, poly, p);
+        const u64 qq = q[p];
+        const u64 xv = x[(size_t)item * x_is + (size_t)poly * x_ps + (size_t)p * n + off];
+        u64 r = shoup(sub_mod(xv, v, qq), w[p], wsh[p], qq);
+        const u64 av = add_a ? add_a[(size_t)item * a_is + (size_t)poly * a_ps + (size_t)p * n + off] : 0;
+        out[(size_t)item * out_is + (size_t)poly * out_ps + (size_t)p * n + off] = addends(r, item, poly, p, off, qq, av);
+    }
+    __device__ __forceinline__ void store2(int z, int li, int, int off, ulonglong2 v) const {
+        int item, poly, p;
+        decode(z, li, item, poly, p);
+        const u64 qq = q[p], wp = w[p], wps = wsh[p];
+        const ulonglong2 xv = ld2(x + (size_t)item * x_is + (size_t)poly * x_ps + (size_t)p * n + off);
+        ulonglong2 av = make_ulonglong2(0, 0);
+        if (add_a) av = ld2(add_a + (size_t)item * a_is + (size_t)poly * a_ps + (size_t)p * n + off);
+        const u64 r0 = addends(shoup(sub_mod(xv.x, v.x, qq), wp, wps, qq), item, poly, p, off, qq, av.x);
+        const u64 r1 = addends(shoup(sub_mod(xv.y, v.y, qq), wp, wps, qq), item, poly, p, off + 1, qq, av.y);
+        st2(out + (size_t)item * out_is + (size_t)poly * out_ps + (size_t)p * n + off, r0, r1);
+    }
+};
+static StCombine st_combine(const helr_ctx* c, u64* out, long long out_is, long long out_ps, const u64* x, long long x_is,
+                            long long x_ps, const u64* w, const u64* wsh, int per_poly) {
+    StCombine f;
+    f.out = out; f.out_is = out_is; f.out_ps = out_ps;
+    f.x = x; f.x_is = x_is; f.x_ps = x_ps;
+    f.w = w; f.wsh = wsh; f.q = c->t.q;
+    f.add_a = nullptr; f.a_is = f.a_ps = 0;
+    f.add_p = nullptr; f.p_is = 0;
+    f.ngal = 0; f.log_n = c->log_n; f.n = c->n; f.per_poly = per_poly;
+    for (int t = 0; t < HELR_MAX_HOIST; t++) f.gal[t] = 1;
+    return f;
+}
 
 static int rescale_dev(helr_ctx* c, const u64* a, long long as, u64* out, long long os, int count, int level,
                        cudaStream_t s) {
@@ -460,15 +517,13 @@ static int rescale_dev(helr_ctx* c, const u64* a, long long as, u64* out, long l
         k_rescale_conv<<<g1, 256, 0, s>>>(r, t, n, l, c->t);
         CHECK_KERNEL("rescale conv");
     }
+    // NTT of the converted limbs; the last pass finishes the rescale in its storer
     LimbMap m = limb_range(0, l);
-    ntt_buffers<false>(c, t, (long long)l * n, t, (long long)l * n, m, items, s);
-    CHECK_LAUNCH("rescale ntt");
-    dim3 g2(blocks_for(n, 256), l, items);
-    {
-        ProfScope ps(PROF_RESCALE, 8.0 * n * items * l * 3, s);
-        k_rescale_final<<<g2, 256, 0, s>>>(a, as, t, out, os, n, L, l, c->qlinv, c->qlinv_sh, c->t);
-        CHECK_KERNEL("rescale final");
-    }
+    LdBuf ld{t, (long long)l * n, m, n};
+    const StCombine st = st_combine(c, out, os, (long long)L * n, a, as, (long long)L * n, c->qlinv + (size_t)l * L,
+                                    c->qlinv_sh + (size_t)l * L, 0);
+    ntt_launch<false>(c, ld, st, t, (long long)l * n, m, items, s);
+    CHECK_LAUNCH("rescale ntt+final");
     return HELR_OK;
 }
 
@@ -532,8 +587,6 @@ struct ModUpArgs {
 };
 // Two consecutive coefficients per thread, 16-byte accesses; register
 // arrays bounded by the template parameter (alpha / K <= MA).
-__device__ __forceinline__ ulonglong2 ld2(const u64* p) { return *reinterpret_cast<const ulonglong2*>(p); }
-__device__ __forceinline__ void st2(u64* p, u64 x, u64 y) { *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(x, y); }
 
 template <int MA>
 __global__ void k_modup(ModUpArgs a, Tables tb) {
@@ -683,35 +736,6 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
     }
 }
 
-__global__ void k_moddown_final(const u64* acc, long long acc_item_stride, const u64* mdc, long long mdc_item_stride,
-                                KsEpilogue ep, int n, int log_n, int nl, int K, int L, const u64* pinv,
-                                const u64* pinv_sh, Tables tb) {
-    const int p = blockIdx.y;
-    const int it = blockIdx.z, b = it >> 1, poly = it & 1;
-    const int ne = nl + K;
-    const u64 q = tb.q[p];
-    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i >= n) return;
-    const u64* ap = acc + (size_t)b * acc_item_stride + ((size_t)poly * ne + p) * n;
-    const u64* mp = mdc + (size_t)b * mdc_item_stride + ((size_t)poly * L + p) * n;
-    u64* op = ep.out + (size_t)b * ep.out_stride + ((size_t)poly * L + p) * n;
-    const ulonglong2 x = ld2(ap + i), c = ld2(mp + i);
-    u64 v0 = shoup(sub_mod(x.x, c.x, q), pinv[p], pinv_sh[p], q);
-    u64 v1 = shoup(sub_mod(x.y, c.y, q), pinv[p], pinv_sh[p], q);
-    if (ep.add_a) {
-        const ulonglong2 y = ld2(ep.add_a + (size_t)b * ep.add_a_stride + ((size_t)poly * L + p) * n + i);
-        v0 = add_mod(v0, y.x, q);
-        v1 = add_mod(v1, y.y, q);
-    }
-    if (ep.add_p && poly == 0) {
-        const u64* pp = ep.add_p + (size_t)b * ep.add_p_stride + (size_t)p * n;
-        for (int t = 0; t < ep.ngal; t++) {
-            v0 = add_mod(v0, pp[galois_perm(i, (u64)ep.gal[t], log_n)], q);
-            v1 = add_mod(v1, pp[galois_perm(i + 1, (u64)ep.gal[t], log_n)], q);
-        }
-    }
-    st2(op + i, v0, v1);
-}
 
 // Loader applying the Galois permutation to a plain buffer (rotation input).
 struct LdPerm {
@@ -822,14 +846,18 @@ static int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const
             mq.off[poly * nl + i] = (unsigned char)(poly * L + i);
             mq.prime[poly * nl + i] = (unsigned char)i;
         }
-    ntt_buffers<false>(c, w.mdc, w.mdc_s, w.mdc, w.mdc_s, mq, B, s);
-    CHECK_LAUNCH("ks moddown ntt");
-    dim3 g2(blocks_for(n / 2, 256), nl, 2 * B);
+    // NTT of the conversion; its last pass applies (acc - conv) * P^-1 and
+    // the epilogue addends while storing (StCombine)
     {
-        ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * nl * (3.0 + (ep.add_a ? 1 : 0) + (ep.add_p ? 0.5 * ep.ngal : 0)), s);
-        k_moddown_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, ep, n, c->log_n, nl, K, L, c->md_pinv,
-                                           c->md_pinv_sh, c->t);
-        CHECK_KERNEL("ks moddown final");
+        LdBuf ld{w.mdc, w.mdc_s, mq, n};
+        StCombine st = st_combine(c, ep.out, ep.out_stride, (long long)L * n, w.acc, w.acc_s, (long long)ne * n,
+                                  c->md_pinv, c->md_pinv_sh, nl);
+        st.add_a = ep.add_a; st.a_is = ep.add_a_stride; st.a_ps = (long long)L * n;
+        st.add_p = ep.add_p; st.p_is = ep.add_p_stride;
+        st.ngal = ep.add_p ? ep.ngal : 0;
+        for (int t = 0; t < HELR_MAX_HOIST; t++) st.gal[t] = ep.gal[t];
+        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s);
+        CHECK_LAUNCH("ks moddown ntt+final");
     }
     return HELR_OK;
 }
@@ -909,19 +937,6 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
             sub_mod(s1, shoup(rr1, mt.mm[p], mt.mms[p], q), q));
     }
 }
-__global__ void k_mdr_final(const u64* acc, long long acc_item_stride, const u64* mdc, long long mdc_item_stride, u64* out,
-                            long long os, int n, int nl, int K, int L, MrTab mt, Tables tb) {
-    const int p = blockIdx.y;
-    const int it = blockIdx.z, b = it >> 1, poly = it & 1;
-    const int ne = nl + K;
-    const u64 q = tb.q[p];
-    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i >= n) return;
-    const ulonglong2 x = ld2(acc + (size_t)b * acc_item_stride + ((size_t)poly * ne + p) * n + i);
-    const ulonglong2 cv = ld2(mdc + (size_t)b * mdc_item_stride + ((size_t)poly * L + p) * n + i);
-    st2(out + (size_t)b * os + ((size_t)poly * L + p) * n + i, shoup(sub_mod(x.x, cv.x, q), mt.mi[p], mt.mis[p], q),
-        shoup(sub_mod(x.y, cv.y, q), mt.mi[p], mt.mis[p], q));
-}
 
 static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, int B, const KsWs& w, cudaStream_t s) {
     const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K, l = level;
@@ -952,13 +967,11 @@ static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, in
             mq.off[poly * l + i] = (unsigned char)(poly * L + i);
             mq.prime[poly * l + i] = (unsigned char)i;
         }
-    ntt_buffers<false>(c, w.mdc, w.mdc_s, w.mdc, w.mdc_s, mq, B, s);
-    CHECK_LAUNCH("mdr ntt");
     {
-        dim3 g2(blocks_for(n / 2, 256), l, 2 * B);
-        ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * l * 3.0, s);
-        k_mdr_final<<<g2, 256, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, out, os, n, nl, K, L, mt, c->t);
-        CHECK_KERNEL("mdr final");
+        LdBuf ld{w.mdc, w.mdc_s, mq, n};
+        const StCombine st = st_combine(c, out, os, (long long)L * n, w.acc, w.acc_s, (long long)ne * n, mt.mi, mt.mis, l);
+        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s);
+        CHECK_LAUNCH("mdr ntt+final");
     }
     return HELR_OK;
 }
