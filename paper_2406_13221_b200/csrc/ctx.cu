@@ -135,6 +135,10 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
     size_t o_itw = put(2 * (size_t)LK * n);
     size_t o_ni = put(LK), o_nis = put(LK), o_i1 = put(LK), o_i1s = put(LK);
     size_t o_one = put(LK), o_t128 = put(LK), o_t128s = put(LK);  // floor(2^64/q); 2^128 mod q (+ Shoup)
+    // fp64 twiddles / constants (bit patterns of doubles) for the fp64 NTT path
+    size_t o_twd = put((size_t)LK * n), o_itwd = put((size_t)LK * n);
+    size_t o_qd = put(LK), o_qinvd = put(LK), o_nid = put(LK), o_i1d = put(LK);
+    auto dbits = [](double v) { u64 b; memcpy(&b, &v, 8); return b; };
     for (int p = 0; p < LK; p++) {
         u64 q = primes[p];
         h[o_q + p] = q;
@@ -159,6 +163,8 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
             h[o_tw + 2 * ((size_t)p * n + k) + 1] = hshoup(w, q);
             h[o_itw + 2 * ((size_t)p * n + k)] = iw;
             h[o_itw + 2 * ((size_t)p * n + k) + 1] = hshoup(iw, q);
+            h[o_twd + (size_t)p * n + k] = dbits((double)w);
+            h[o_itwd + (size_t)p * n + k] = dbits((double)iw);
         }
         u64 ni = hinv((u64)n, q);
         h[o_ni + p] = ni;
@@ -166,6 +172,10 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
         u64 i1 = hmul(h[o_itw + 2 * ((size_t)p * n + 1)], ni, q);
         h[o_i1 + p] = i1;
         h[o_i1s + p] = hshoup(i1, q);
+        h[o_qd + p] = dbits((double)q);
+        h[o_qinvd + p] = dbits(1.0 / (double)q);
+        h[o_nid + p] = dbits((double)ni);
+        h[o_i1d + p] = dbits((double)i1);
     }
     // rescale constants
     size_t o_ql = put((size_t)L * L), o_qls = put((size_t)L * L);
@@ -278,8 +288,10 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
         cudaFree(c->d_tab); delete c; return HELR_ECUDA;
     }
     const u64* d = c->d_tab;
+    auto dp = [&](size_t o) { return reinterpret_cast<const double*>(d + o); };
     c->t = Tables{d + o_q, d + o_b1, d + o_b0, d + o_tw, d + o_itw,
-                  d + o_ni, d + o_nis, d + o_i1, d + o_i1s, log_n, n, L, K, alpha, c->beta};
+                  d + o_ni, d + o_nis, d + o_i1, d + o_i1s, log_n, n, L, K, alpha, c->beta,
+                  dp(o_twd), dp(o_itwd), dp(o_qd), dp(o_qinvd), dp(o_nid), dp(o_i1d)};
     c->qlinv = d + o_ql; c->qlinv_sh = d + o_qls;
     c->md_phinv = d + o_phi; c->md_phinv_sh = d + o_phis;
     c->md_phmod = d + o_phm; c->md_phmod_sh = d + o_phms;

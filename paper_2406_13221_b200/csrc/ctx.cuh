@@ -22,6 +22,13 @@ struct Tables {
     const u64* itw1n;    // [LK]  psi^-brv(1) * N^-1  (last inverse stage)
     const u64* itw1n_sh;
     int log_n, n, L, K, alpha, beta;
+    // fp64 NTT path for primes < 2^41 (ntt.cuh): the same twiddles as exact doubles
+    const double* twd;    // [LK][N]  psi^brv(k)
+    const double* itwd;   // [LK][N]  psi^-brv(k)
+    const double* qd;     // [LK]  q
+    const double* qinvd;  // [LK]  fl(1 / q)
+    const double* nid;    // [LK]  N^-1
+    const double* i1d;    // [LK]  psi^-brv(1) N^-1
 };
 
 // Limb selection for batched kernels: limb i of item z lives at

@@ -23,6 +23,8 @@
 // rescale, ModUp and ModDown fuse their basis conversions into the NTT
 // instead of making extra passes over HBM.
 #pragma once
+#include <type_traits>
+
 #include "ctx.cuh"
 #include "prof.cuh"
 
@@ -137,23 +139,123 @@ __device__ __forceinline__ void inv_last_h(int h, u64 (&x)[R], u64 ni, u64 nis, 
     }
 }
 
-template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, class Ld, class St>
-__global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R), ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 256 ? 4 : 1)
-ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
+// ---- fp64 path for primes < 2^41 ------------------------------------------
+// Residues of primes below 2^41 are exact doubles.  A twiddle product is
+// computed on the FP64 pipe (idle otherwise; DFMA issues at the IMAD rate,
+// 2.5x IMAD.WIDE): p = fl(a w), e = fma(a, w, -p) (exact), h = rint(p / q) by
+// the 1.5 2^52 trick, r = fma(-h, q, p) + e = a w - h q exactly, |r| < 0.6 q.
+// Signed values grow by < 0.6 q per forward stage and at most double per
+// inverse stage; a pass (<= 8 stages) starting from canonical inputs stays
+// below 2^50, so every intermediate is an exact integer-valued double, and
+// every pass ends with an exact reduction to [0, q).  Identical residues to
+// the integer path and the oracle.
+constexpr double NTT_MAGIC = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double NTT_TWO52 = 4503599627370496.0;  // 2^52
+struct DblC { double q, qinv; };
+__device__ __forceinline__ double drint(double x) { return __dsub_rn(__dadd_rn(x, NTT_MAGIC), NTT_MAGIC); }
+__device__ __forceinline__ double mulmod_d(double a, double w, const DblC& c) {
+    const double p = __dmul_rn(a, w);
+    const double e = __fma_rn(a, w, -p);
+    const double h = drint(__dmul_rn(p, c.qinv));
+    return __dadd_rn(__fma_rn(-h, c.q, p), e);
+}
+__device__ __forceinline__ double u2d(u64 x) {  // x < 2^52
+    return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), NTT_TWO52);
+}
+__device__ __forceinline__ u64 d2u_canon(double x, const DblC& c) {  // integer-valued |x| < 2^50 -> [0, q)
+    double r = __fma_rn(-drint(__dmul_rn(x, c.qinv)), c.q, x);
+    r = r < 0.0 ? __dadd_rn(r, c.q) : r;
+    return (u64)__double_as_longlong(__dadd_rn(r, NTT_TWO52)) & 0x000FFFFFFFFFFFFFull;
+}
+template <int R, int H>
+__device__ __forceinline__ void fwd_stage_d(double (&x)[R], const double* __restrict__ W, int tb0, const DblC& c) {
+#pragma unroll
+    for (int j = 0; j < (R >> (H + 1)); j++) {
+        const double w = __ldg(W + tb0 + j);
+#pragma unroll
+        for (int t = 0; t < (1 << H); t++) {
+            const int i = (j << (H + 1)) + t;
+            const double u = x[i], v = mulmod_d(x[i + (1 << H)], w, c);
+            x[i] = __dadd_rn(u, v);
+            x[i + (1 << H)] = __dsub_rn(u, v);
+        }
+    }
+}
+template <int R, int H>
+__device__ __forceinline__ void inv_stage_d(double (&x)[R], const double* __restrict__ W, int tb0, const DblC& c) {
+#pragma unroll
+    for (int j = 0; j < (R >> (H + 1)); j++) {
+        const double w = __ldg(W + tb0 + j);
+#pragma unroll
+        for (int t = 0; t < (1 << H); t++) {
+            const int i = (j << (H + 1)) + t;
+            const double u = x[i], v = x[i + (1 << H)];
+            x[i] = __dadd_rn(u, v);
+            x[i + (1 << H)] = mulmod_d(__dsub_rn(u, v), w, c);
+        }
+    }
+}
+template <int R, int H>
+__device__ __forceinline__ void inv_last_stage_d(double (&x)[R], double ni, double wl, const DblC& c) {
+#pragma unroll
+    for (int i = 0; i < R; i++) {
+        if (i & (1 << H)) continue;
+        const double u = x[i], v = x[i + (1 << H)];
+        x[i] = mulmod_d(__dadd_rn(u, v), ni, c);
+        x[i + (1 << H)] = mulmod_d(__dsub_rn(u, v), wl, c);
+    }
+}
+template <int R>
+__device__ __forceinline__ void fwd_stage_dh(int h, double (&x)[R], const double* W, int tb0, const DblC& c) {
+    switch (h) {
+        case 0: fwd_stage_d<R, 0>(x, W, tb0, c); break;
+        case 1: if constexpr (R > 2) fwd_stage_d<R, 1>(x, W, tb0, c); break;
+        case 2: if constexpr (R > 4) fwd_stage_d<R, 2>(x, W, tb0, c); break;
+        default: if constexpr (R > 8) fwd_stage_d<R, 3>(x, W, tb0, c); break;
+    }
+}
+template <int R>
+__device__ __forceinline__ void inv_stage_dh(int h, double (&x)[R], const double* W, int tb0, const DblC& c) {
+    switch (h) {
+        case 0: inv_stage_d<R, 0>(x, W, tb0, c); break;
+        case 1: if constexpr (R > 2) inv_stage_d<R, 1>(x, W, tb0, c); break;
+        case 2: if constexpr (R > 4) inv_stage_d<R, 2>(x, W, tb0, c); break;
+        default: if constexpr (R > 8) inv_stage_d<R, 3>(x, W, tb0, c); break;
+    }
+}
+template <int R>
+__device__ __forceinline__ void inv_last_dh(int h, double (&x)[R], double ni, double wl, const DblC& c) {
+    switch (h) {
+        case 0: inv_last_stage_d<R, 0>(x, ni, wl, c); break;
+        case 1: if constexpr (R > 2) inv_last_stage_d<R, 1>(x, ni, wl, c); break;
+        case 2: if constexpr (R > 4) inv_last_stage_d<R, 2>(x, ni, wl, c); break;
+        default: if constexpr (R > 8) inv_last_stage_d<R, 3>(x, ni, wl, c); break;
+    }
+}
+
+// Primes below this bound take the fp64 path (uniform per CTA: one limb per CTA).
+constexpr u64 NTT_DBL_BOUND = 1ull << 41;
+
+template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, bool DBL, class Ld, class St>
+__device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
+                                         const NttPassArgs& a, u64* sm) {
     using S = NttShape<LOG_T, LOG_R>;
     constexpr int T = S::T, R = S::R, NG = S::NG;
     constexpr int TPS = T / R;  // threads per sub-transform
     constexpr int SROW = IS_COL ? (COLS + 1) : (T + T / 16);
-    __shared__ u64 sm[IS_COL ? T * (COLS + 1) : COLS * (T + T / 16)];
+    using V = typename std::conditional<DBL, double, u64>::type;
 
     const int li = blockIdx.y;
     const int z = blockIdx.z;
     const int prime = map.prime[li];
     const u64 q = tb.q[prime];
-    const u64 q2 = 4 * q;  // lazy half-range (see fwd_stage)
+    const u64 q2 = 4 * q;  // integer path: lazy half-range (see fwd_stage)
+    DblC dc;
+    if constexpr (DBL) dc = DblC{tb.qd[prime], tb.qinvd[prime]};
     const int n = 1 << a.log_n;
     const int s2 = a.log_n - LOG_T;  // used by column passes
     const ulonglong2* W2 = reinterpret_cast<const ulonglong2*>(INV ? tb.itw : tb.tw) + (size_t)prime * n;
+    const double* WD = (INV ? tb.itwd : tb.twd) + (size_t)prime * n;
 
     const int tid = threadIdx.x;
     int cc, s;
@@ -169,8 +271,20 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     auto sidx = [&](int k) -> int {
         return IS_COL ? (k * SROW + cc) : (cc * SROW + k + (k >> 4));
     };
+    auto in_v = [&](u64 v) -> V {
+        if constexpr (DBL) return u2d(v);
+        else return v;
+    };
+    auto to_sm = [&](V v) -> u64 {
+        if constexpr (DBL) return (u64)__double_as_longlong(v);
+        else return v;
+    };
+    auto from_sm = [&](u64 v) -> V {
+        if constexpr (DBL) return __longlong_as_double((long long)v);
+        else return v;
+    };
 
-    u64 x[R];
+    V x[R];
 #pragma unroll
     for (int g = 0; g < NG; g++) {
         // free index bits of this register group: [lo, lo + LOG_R)
@@ -178,25 +292,46 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
                             : ((g * LOG_R < LOG_T - LOG_R) ? g * LOG_R : LOG_T - LOG_R);
         const int base = spread_index(s, lo, LOG_R);
         if (g == 0) {
-            if constexpr (!IS_COL && has_vec<Ld>::value) {
+            if constexpr (!IS_COL && has_tile<Ld>::value) {
+                if (lo == 0) {
+                    // coalesced prologue: the CTA's T * COLS contiguous inputs
+                    // through shared memory (each thread then takes R in a row)
+                    constexpr int TOT = T * COLS;
+                    const int nthr = T * COLS / R;
+#pragma unroll 4
+                    for (int e = 2 * tid; e < TOT; e += 2 * nthr) {
+                        const int c2 = e >> LOG_T, k = e & (T - 1);
+                        const ulonglong2 v = ld.load2(z, li, prime, ((blockIdx.x * COLS + c2) << LOG_T) + k);
+                        sm[c2 * SROW + k + (k >> 4)] = v.x;
+                        sm[c2 * SROW + k + 1 + ((k + 1) >> 4)] = v.y;
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int i = 0; i < R; i++) x[i] = in_v(sm[sidx(base + i)]);
+                    __syncthreads();
+                } else {
+#pragma unroll
+                    for (int i = 0; i < R; i++) x[i] = in_v(ld(z, li, prime, goff(base + (i << lo))));
+                }
+            } else if constexpr (!IS_COL && has_vec<Ld>::value) {
                 if (lo == 0) {
 #pragma unroll
                     for (int i = 0; i < R; i += 2) {
                         const ulonglong2 v = ld.load2(z, li, prime, goff(base + i));
-                        x[i] = v.x;
-                        x[i + 1] = v.y;
+                        x[i] = in_v(v.x);
+                        x[i + 1] = in_v(v.y);
                     }
                 } else {
 #pragma unroll
-                    for (int i = 0; i < R; i++) x[i] = ld(z, li, prime, goff(base + (i << lo)));
+                    for (int i = 0; i < R; i++) x[i] = in_v(ld(z, li, prime, goff(base + (i << lo))));
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < R; i++) x[i] = ld(z, li, prime, goff(base + (i << lo)));
+                for (int i = 0; i < R; i++) x[i] = in_v(ld(z, li, prime, goff(base + (i << lo))));
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < R; i++) x[i] = sm[sidx(base + (i << lo))];
+            for (int i = 0; i < R; i++) x[i] = from_sm(sm[sidx(base + (i << lo))]);
             if (NG > 2) __syncthreads();
         }
         if (!INV) {
@@ -205,7 +340,9 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
 #pragma unroll
             for (int qb = qhi; qb >= qlo; qb--) {
                 const int ls = LOG_T - 1 - qb;
-                fwd_stage_h<R>(qb - lo, x, W2, (wrow << ls) + (base >> (qb + 1)), q, q2);
+                const int t0 = (wrow << ls) + (base >> (qb + 1));
+                if constexpr (DBL) fwd_stage_dh<R>(qb - lo, x, WD, t0, dc);
+                else fwd_stage_h<R>(qb - lo, x, W2, t0, q, q2);
             }
         } else {
             const int qlo = g * LOG_R;
@@ -214,27 +351,36 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
             for (int qb = qlo; qb <= qhi; qb++) {
                 const int ls = LOG_T - 1 - qb;
                 if (a.st0 == 0 && ls == 0) {
-                    inv_last_h<R>(qb - lo, x, tb.ninv[prime], tb.ninv_sh[prime], tb.itw1n[prime], tb.itw1n_sh[prime],
-                                  q, q2);
+                    if constexpr (DBL) inv_last_dh<R>(qb - lo, x, tb.nid[prime], tb.i1d[prime], dc);
+                    else inv_last_h<R>(qb - lo, x, tb.ninv[prime], tb.ninv_sh[prime], tb.itw1n[prime],
+                                       tb.itw1n_sh[prime], q, q2);
                 } else {
-                    inv_stage_h<R>(qb - lo, x, W2, (wrow << ls) + (base >> (qb + 1)), q, q2);
+                    const int t0 = (wrow << ls) + (base >> (qb + 1));
+                    if constexpr (DBL) inv_stage_dh<R>(qb - lo, x, WD, t0, dc);
+                    else inv_stage_h<R>(qb - lo, x, W2, t0, q, q2);
                 }
             }
         }
         if (g == NG - 1) {
+            u64 y[R];
 #pragma unroll
             for (int i = 0; i < R; i++) {
-                if (a.final_out) {  // forward [0, 8q), inverse [0, 4q) -> [0, q)
+                if constexpr (DBL) {
+                    y[i] = d2u_canon(x[i], dc);  // every fp64 pass ends canonical
+                } else {
                     u64 v = x[i];
-                    if (!INV) v = v >= q2 ? v - q2 : v;
-                    v = v >= 2 * q ? v - 2 * q : v;
-                    x[i] = v >= q ? v - q : v;
+                    if (a.final_out) {  // forward [0, 8q), inverse [0, 4q) -> [0, q)
+                        if (!INV) v = v >= q2 ? v - q2 : v;
+                        v = v >= 2 * q ? v - 2 * q : v;
+                        v = v >= q ? v - q : v;
+                    }
+                    y[i] = v;
                 }
             }
             if constexpr (!IS_COL && has_tile<St>::value) {
                 if (NG > 1) __syncthreads();  // this group's shared-memory reads are done
 #pragma unroll
-                for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = x[i];
+                for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = y[i];
                 __syncthreads();
                 constexpr int TOT = T * COLS;
                 const int nthr = T * COLS / R;
@@ -247,29 +393,41 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
             } else if constexpr (!IS_COL && has_vec<St>::value) {
                 if (lo == 0) {
 #pragma unroll
-                    for (int i = 0; i < R; i += 2) st.store2(z, li, prime, goff(base + i), make_ulonglong2(x[i], x[i + 1]));
+                    for (int i = 0; i < R; i += 2) st.store2(z, li, prime, goff(base + i), make_ulonglong2(y[i], y[i + 1]));
                 } else {
 #pragma unroll
-                    for (int i = 0; i < R; i++) st(z, li, prime, goff(base + (i << lo)), x[i]);
+                    for (int i = 0; i < R; i++) st(z, li, prime, goff(base + (i << lo)), y[i]);
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < R; i++) st(z, li, prime, goff(base + (i << lo)), x[i]);
+                for (int i = 0; i < R; i++) st(z, li, prime, goff(base + (i << lo)), y[i]);
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = x[i];
+            for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = to_sm(x[i]);
             __syncthreads();
         }
     }
 }
 
+template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, class Ld, class St>
+__global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R), ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 256 ? 4 : 1)
+ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
+    constexpr int T = 1 << LOG_T;
+    __shared__ u64 sm[IS_COL ? T * (COLS + 1) : COLS * (T + T / 16)];
+    if (tb.q[map.prime[blockIdx.y]] < NTT_DBL_BOUND)
+        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, true>(ld, st, tb, map, a, sm);
+    else
+        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, false>(ld, st, tb, map, a, sm);
+}
+
 // ---- plain functors: strided limb buffers -------------------------------
 #ifndef HELR_STBUF_TILE
-#define HELR_STBUF_TILE false
+#define HELR_STBUF_TILE true
 #endif
 struct LdBuf {
     static constexpr bool kVec = true;
+    static constexpr bool kTile = HELR_STBUF_TILE;
     const u64* base;
     long long item_stride;
     LimbMap map;  // copy of the offsets (small)

@@ -51,8 +51,11 @@ def timed(fn, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
+SCALE_BITS = 50
+
+
 def run(log_n, L, dnum, batch, ops):
-    ck = CkksParams.generate(log_n=log_n, n_q=L, dnum=dnum, scale_bits=50)
+    ck = CkksParams.generate(log_n=log_n, n_q=L, dnum=dnum, scale_bits=SCALE_BITS)
     ctx = GpuContext(ck, seed=3, max_batch=batch)
     n, K = ck.n, ck.K
     beta = -(-L // ck.alpha)
@@ -110,7 +113,10 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--json", default=None)
     ap.add_argument("--ops", default="ntt,mul,rescale,rotate,rotsum")
+    ap.add_argument("--scale-bits", type=int, default=50, help="scaling-prime size (< 41 bits: fp64 NTT path)")
     a = ap.parse_args()
+    global SCALE_BITS
+    SCALE_BITS = a.scale_bits
     ops = a.ops.split(",")
     P = peak()
     grid = [(16, 8, 3, 8), (16, 8, 3, 64)] if a.quick else [
@@ -123,7 +129,7 @@ def main():
         try:
             for name, ms, by in run(ln, L, d, b, ops):
                 gbs = by / (ms / 1e3) / 1e9
-                row = dict(op=name, log_n=ln, L=L, dnum=d, batch=b, ms=ms, gbs=gbs, frac=gbs / P)
+                row = dict(op=name, log_n=ln, L=L, dnum=d, batch=b, scale_bits=SCALE_BITS, ms=ms, gbs=gbs, frac=gbs / P)
                 rows.append(row)
                 print(json.dumps(row), flush=True)
         except Exception as exc:  # report and continue the sweep
