@@ -13,8 +13,10 @@
  *    success or a negative HELR_E* code, with a message retrievable through
  *    helr_last_error().  Every call is asynchronous on the given stream.
  *  - Ring: N = 2^log_n, primes[0..L-1] = q_0..q_{L-1} (ciphertext chain),
- *    primes[L..L+K-1] = p_0..p_{K-1} (special primes, K = alpha =
- *    ceil(L/dnum)).  All primes < 2^61, = 1 mod 2N.
+ *    primes[L..L+K-1] = p_0..p_{K-1} (special primes; key-switching digits
+ *    hold alpha = ceil(L/dnum) limbs, P = prod p_k should exceed the largest
+ *    digit modulus).  All primes < 2^61, = 1 mod 2N; primes < 2^41 take the
+ *    fp64 NTT path.
  *  - Polynomials are limb-major u64[limbs][N] of canonical residues in
  *    [0, q), in negacyclic NTT (evaluation) form unless stated otherwise.
  *    NTT slot i holds a(psi^(2*brv(i)+1)).

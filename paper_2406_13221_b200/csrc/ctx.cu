@@ -104,7 +104,6 @@ extern "C" int helr_ctx_create(helr_ctx** out, int log_n, int L, int K, int dnum
     if (L < 2 || K < 1 || L + K > HELR_MAXP) { set_error("bad prime counts"); return HELR_EINVAL; }
     if (dnum < 1 || dnum > L) { set_error("bad dnum"); return HELR_EINVAL; }
     const int alpha = (L + dnum - 1) / dnum;
-    if (K != alpha) { set_error("K must equal alpha = ceil(L/dnum)"); return HELR_EINVAL; }
     if (max_batch < 1) max_batch = 1;
     const int n = 1 << log_n;
     for (int i = 0; i < L + K; i++) {

@@ -9,8 +9,9 @@ fields, validation messages and ``from_file`` JSON keys, because the driver
 ``CkksParams`` is new.  It fixes the real ring: N = 2**log_n, a modulus
 chain q_0 (about 2**60) and q_1..q_{L-1} (about 2**log_scale, alternately
 just above and below so the per-level scale stays close to 2**log_scale),
-K special primes p_k (about 2**61) for hybrid key switching with ``dnum``
-digits of ``alpha`` limbs, and one primitive 2N-th root of unity per prime.
+K special primes p_k (about 2**40 by default, or 2**61) for hybrid key
+switching with ``dnum`` digits of ``alpha`` limbs, and one primitive 2N-th
+root of unity per prime.
 All primes are below 2**61 so the lazy [0, 8q) NTT butterflies (approximate
 Shoup quotients) and the 128-bit key-product accumulators never overflow.  Everything here is plain integer arithmetic and
 deterministic, so the device library and the CPU oracle are handed the
@@ -178,7 +179,8 @@ class CkksParams:
     """A concrete RNS-CKKS ring.
 
     q: the L ciphertext primes (q[0] is the decryption prime, q[1:] are
-    rescaling primes); p: the K = alpha special primes; dnum: number of
+    rescaling primes); p: the K special primes (product P well above the
+    largest key-switching digit modulus); dnum: number of
     key-switching digits at the top level.  ``scale_bits`` is the nominal
     log2 of the fresh encoding scale.  ``cbd_eta`` is the centred-binomial
     error parameter (variance eta/2; 21 gives sigma ~ 3.24).
@@ -200,8 +202,8 @@ class CkksParams:
             raise ValueError("need at least two ciphertext primes")
         if self.dnum < 1 or self.dnum > len(self.q):
             raise ValueError(f"dnum must be in [1, {len(self.q)}], got {self.dnum}")
-        if len(self.p) != self.alpha:
-            raise ValueError(f"need alpha = {self.alpha} special primes, got {len(self.p)}")
+        if len(self.p) < 1 or len(self.q) + len(self.p) > 64:
+            raise ValueError(f"need 1..{64 - len(self.q)} special primes, got {len(self.p)}")
         m = 2 << self.log_n
         for x in tuple(self.q) + tuple(self.p):
             if x >= (1 << 61) or (x - 1) % m or not is_prime(x):
@@ -218,11 +220,20 @@ class CkksParams:
 
     @classmethod
     def generate(cls, log_n: int, n_q: int, dnum: int = 3, scale_bits: int = 40,
-                 q0_bits: int = 60, p_bits: int = 61, cbd_eta: int = 21, secret_hw: int = 64) -> "CkksParams":
+                 q0_bits: int = 60, p_bits: int = 40, cbd_eta: int = 21, secret_hw: int = 64,
+                 n_special: int = None, ks_margin_bits: int = 20) -> "CkksParams":
+        """Special primes: ``n_special`` of ``p_bits`` bits, by default the
+        fewest whose product exceeds the largest digit modulus (the one
+        holding q_0) by ``ks_margin_bits`` — alpha primes of 61 bits, or
+        alpha + 1 of 40 bits.  40-bit specials (the default) let every limb
+        but q_0 take the fp64 NTT path (primes < 2^41)."""
         alpha = -(-n_q // dnum)
+        if n_special is None:
+            digit_bits = q0_bits + (min(alpha, n_q) - 1) * scale_bits
+            n_special = -(-(digit_bits + ks_margin_bits) // p_bits)
         q0 = ntt_primes(log_n, q0_bits, 1, mode="below")
         scaling = ntt_primes(log_n, scale_bits, n_q - 1, mode="closest", exclude=tuple(q0))
-        special = ntt_primes(log_n, p_bits, alpha, mode="below", exclude=tuple(q0 + scaling))
+        special = ntt_primes(log_n, p_bits, n_special, mode="below", exclude=tuple(q0 + scaling))
         return cls(log_n=log_n, q=tuple(q0 + scaling), p=tuple(special), dnum=dnum,
                    scale_bits=scale_bits, cbd_eta=cbd_eta, secret_hw=secret_hw)
 

@@ -63,7 +63,12 @@ def test_heparams_surface():
 
 def test_ckks_params_views():
     ck = CkksParams.generate(log_n=16, n_q=8, dnum=3)
-    assert (ck.L, ck.K, ck.alpha) == (8, 3, 3)
+    # 40-bit special primes: alpha + 1 of them cover the q_0 digit (2^140) with margin
+    assert (ck.L, ck.K, ck.alpha) == (8, 4, 3)
+    assert all(p < 2 ** 41 for p in ck.p) and np.prod([float(p) for p in ck.p]) > 2.0 ** 159
+    ck61 = CkksParams.generate(log_n=16, n_q=8, dnum=3, p_bits=61)
+    assert (ck61.K, ck61.alpha) == (3, 3) and all(p < 2 ** 61 for p in ck61.p)
+    assert CkksParams.generate(log_n=16, n_q=8, dnum=2).K == 5
     hp = ck.he_params()
     assert hp.log_q == 40 * 8 and hp.log_delta == 40 == hp.log_delta_c
     assert ck.level_bits(ck.top_level) == hp.log_q

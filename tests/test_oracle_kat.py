@@ -51,10 +51,17 @@ def test_prng_pinned():
 def test_params_chain():
     for P in (SMALL, MID):
         for q in P.primes:
-            assert is_prime(q) and q < 2 ** 62 and (q - 1) % (2 * P.n) == 0
+            assert is_prime(q) and q < 2 ** 61 and (q - 1) % (2 * P.n) == 0
             psi = P.psi[P.primes.index(q)]
             assert pow(psi, P.n, q) == q - 1
-        assert P.K == P.alpha
+        # P exceeds the largest digit modulus (the one holding q_0)
+        digit = 1
+        for q in P.q[:P.alpha]:
+            digit *= q
+        prod_p = 1
+        for p in P.p:
+            prod_p *= p
+        assert prod_p > digit
         s = P.level_scales
         for lvl in range(1, P.L):
             assert s[lvl - 1] == pytest.approx(s[lvl] ** 2 / P.q[lvl], rel=1e-15)
