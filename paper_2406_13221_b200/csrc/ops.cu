@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -1053,13 +1054,42 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int HOIST_T = 128;     // threads per block (coefficients per tile)
 constexpr int HOIST_STAGES = 3;  // steps in flight per thread
 
+// fp64 multiply-accumulate for limbs whose prime is below 2^41: operands are
+// split at bit 21 into exact doubles (< 2^21), the four partial products
+// (< 2^42) accumulate exactly in three doubles for up to 2^11 terms (every
+// hoisted group has at most 31 * 8), and the sum is reassembled as a 128-bit
+// integer once per output.  DFMA issues at 2.5x the IMAD.WIDE rate on a pipe
+// the integer path leaves idle.
+struct dacc { double hh, mid, ll; };
+__device__ __forceinline__ void split21(u64 x, double& h, double& l) {
+    h = u2d(x >> 21);
+    l = u2d(x & 0x1FFFFFull);
+}
+__device__ __forceinline__ void mac_d(dacc& a, double xh, double xl, double yh, double yl) {
+    a.hh = __fma_rn(xh, yh, a.hh);
+    a.mid = __fma_rn(xh, yl, a.mid);
+    a.mid = __fma_rn(xl, yh, a.mid);
+    a.ll = __fma_rn(xl, yl, a.ll);
+}
+__device__ __forceinline__ u64 dexact(double x) {  // integer-valued 0 <= x < 2^52
+    return (u64)__double_as_longlong(__dadd_rn(x, NTT_TWO52)) & 0x000FFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ u128acc dresolve(const dacc& a) {  // hh 2^42 + mid 2^21 + ll
+    const u64 H = dexact(a.hh), M = dexact(a.mid), Lo = dexact(a.ll);
+    u128acc r{H << 42, H >> 22};
+    const u64 m_lo = M << 21, m_hi = M >> 43;
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r.lo), "+l"(r.hi) : "l"(m_lo), "l"(m_hi));
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(r.lo), "+l"(r.hi) : "l"(Lo));
+    return r;
+}
+
 // grid: x = coefficient tile * chunks + chunk (chunks of NB ciphertexts share
 // the tile's key words through L2 at the same time), y = extended limb e.
-template <int ND, int NB>
-__global__ void __launch_bounds__(HOIST_T, 3)
-k_ks_inner_hoisted(const u64* __restrict__ ext, long long ext_item_stride, long long ext_digit_stride, HoistKeys hk,
-                   u64* acc, long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK, int B,
-                   int nchunks, int fold, Tables tb, const u64* one_sh) {
+template <int ND, int NB, bool DBL>
+__device__ __forceinline__ void hoist_body(const u64* __restrict__ ext, long long ext_item_stride,
+                                           long long ext_digit_stride, const HoistKeys& hk, u64* acc,
+                                           long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK,
+                                           int B, int nchunks, int fold, const Tables& tb, const u64* one_sh) {
     constexpr int W = (2 + NB) * ND;  // words per thread per stage
     constexpr int S = HOIST_STAGES;
     extern __shared__ u64 hsm[];
@@ -1099,39 +1129,64 @@ k_ks_inner_hoisted(const u64* __restrict__ ext, long long ext_item_stride, long 
         }
         cp_async_commit();  // empty groups keep the wait count uniform
     };
-    macc a0[NB], a1[NB];
+    using Acc = typename std::conditional<DBL, dacc, macc>::type;
+    Acc a0[NB], a1[NB];
 #pragma unroll
-    for (int b = 0; b < NB; b++) a0[b] = a1[b] = macc{0, 0, 0, 0};
+    for (int b = 0; b < NB; b++) {
+        if constexpr (DBL) a0[b] = a1[b] = dacc{0.0, 0.0, 0.0};
+        else a0[b] = a1[b] = macc{0, 0, 0, 0};
+    }
 #pragma unroll
     for (int t = 0; t < S - 1; t++) issue(t);
     int run = 0;
     for (int t = 0; t < hk.nsteps; t++) {
         issue(t + S - 1);
         cp_async_wait<S - 1>();
-        if (run == fold) {  // fold into a residue before the 128-bit sum can overflow
+        const int stage = t % S;
+        if constexpr (DBL) {
+            double k0h[ND], k0l[ND], k1h[ND], k1l[ND];
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                split21(*slot(stage, j), k0h[j], k0l[j]);
+                split21(*slot(stage, ND + j), k1h[j], k1l[j]);
+            }
 #pragma unroll
             for (int b = 0; b < NB; b++) {
-                a0[b] = macc{reduce128(resolve(a0[b]), q, r1, r0, osh), 0, 0, 0};
-                a1[b] = macc{reduce128(resolve(a1[b]), q, r1, r0, osh), 0, 0, 0};
+                if (b < nb) {
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        double uh, ul;
+                        split21(*slot(stage, 2 * ND + b * ND + j), uh, ul);
+                        mac_d(a0[b], uh, ul, k0h[j], k0l[j]);
+                        mac_d(a1[b], uh, ul, k1h[j], k1l[j]);
+                    }
+                }
             }
-            run = 0;
-        }
-        run++;
-        const int stage = t % S;
-        u64 k0[ND], k1[ND];
+        } else {
+            if (run == fold) {  // fold into a residue before the 128-bit sum can overflow
 #pragma unroll
-        for (int j = 0; j < ND; j++) {
-            k0[j] = *slot(stage, j);
-            k1[j] = *slot(stage, ND + j);
-        }
+                for (int b = 0; b < NB; b++) {
+                    a0[b] = macc{reduce128(resolve(a0[b]), q, r1, r0, osh), 0, 0, 0};
+                    a1[b] = macc{reduce128(resolve(a1[b]), q, r1, r0, osh), 0, 0, 0};
+                }
+                run = 0;
+            }
+            run++;
+            u64 k0[ND], k1[ND];
 #pragma unroll
-        for (int b = 0; b < NB; b++) {
-            if (b < nb) {
+            for (int j = 0; j < ND; j++) {
+                k0[j] = *slot(stage, j);
+                k1[j] = *slot(stage, ND + j);
+            }
 #pragma unroll
-                for (int j = 0; j < ND; j++) {
-                    const u64 u = *slot(stage, 2 * ND + b * ND + j);
-                    mac_split(a0[b], u, k0[j]);
-                    mac_split(a1[b], u, k1[j]);
+            for (int b = 0; b < NB; b++) {
+                if (b < nb) {
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const u64 u = *slot(stage, 2 * ND + b * ND + j);
+                        mac_split(a0[b], u, k0[j]);
+                        mac_split(a1[b], u, k1[j]);
+                    }
                 }
             }
         }
@@ -1141,10 +1196,30 @@ k_ks_inner_hoisted(const u64* __restrict__ ext, long long ext_item_stride, long 
     for (int b = 0; b < NB; b++) {
         if (b < nb) {
             u64* ap = acc + (size_t)(b0 + b) * acc_item_stride;
-            ap[(size_t)e * n + i] = reduce128(resolve(a0[b]), q, r1, r0, osh);
-            ap[((size_t)(nl + K) + e) * n + i] = reduce128(resolve(a1[b]), q, r1, r0, osh);
+            if constexpr (DBL) {
+                ap[(size_t)e * n + i] = reduce128(dresolve(a0[b]), q, r1, r0, osh);
+                ap[((size_t)(nl + K) + e) * n + i] = reduce128(dresolve(a1[b]), q, r1, r0, osh);
+            } else {
+                ap[(size_t)e * n + i] = reduce128(resolve(a0[b]), q, r1, r0, osh);
+                ap[((size_t)(nl + K) + e) * n + i] = reduce128(resolve(a1[b]), q, r1, r0, osh);
+            }
         }
     }
+}
+
+template <int ND, int NB>
+__global__ void __launch_bounds__(HOIST_T, 3)
+k_ks_inner_hoisted(const u64* __restrict__ ext, long long ext_item_stride, long long ext_digit_stride, HoistKeys hk,
+                   u64* acc, long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK, int B,
+                   int nchunks, int fold, Tables tb, const u64* one_sh) {
+    const int e = blockIdx.y;
+    const int p = e < nl ? e : L + (e - nl);
+    if (tb.q[p] < NTT_DBL_BOUND)  // uniform per CTA (one limb per CTA)
+        hoist_body<ND, NB, true>(ext, ext_item_stride, ext_digit_stride, hk, acc, acc_item_stride, n, log_n, nl, K, L,
+                                 LK, B, nchunks, fold, tb, one_sh);
+    else
+        hoist_body<ND, NB, false>(ext, ext_item_stride, ext_digit_stride, hk, acc, acc_item_stride, n, log_n, nl, K,
+                                  L, LK, B, nchunks, fold, tb, one_sh);
 }
 
 // Steps per 128-bit accumulation run: a run adds fold*nd products (each <
