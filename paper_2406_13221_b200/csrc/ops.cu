@@ -863,20 +863,34 @@ static int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const
     return HELR_OK;
 }
 
-static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, const KsEpilogue& ep, int B,
-                           const KsWs& w, cudaStream_t s) {
+struct HoistKeys {
+    int nsteps;
+    const u64* key[HELR_MAX_HOIST];
+    long long gal[HELR_MAX_HOIST];
+};
+// single-key inner product (relinearisation / one rotation): with one key
+// there is no step loop to prefetch across, so the 2-coefficient, ciphertext-
+// row kernel (k_ks_inner) is faster than the hoisted kernel here
+static int key_inner_single(helr_ctx* c, const KsWs& w, const u64* evk, int B, int level, const u64* dadd,
+                            long long dadd_is, cudaStream_t s) {
     const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
     const int nd = (nl + c->alpha - 1) / c->alpha;
+    const int by = B < 8 ? B : 8;
+    dim3 g(blocks_for(n / 2, 64), ne, (B + by - 1) / by);
+    ProfScope ps(PROF_INNER, 8.0 * n * ((double)B * nd * ne + 2.0 * nd * ne + 2.0 * B * ne + (dadd ? 2.0 * B * nl : 0.0)),
+                 s);
+    k_ks_inner<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B,
+                                          c->t, dadd, dadd_is, c->pmod, c->pmod_sh);
+    CHECK_KERNEL("ks inner");
+    return HELR_OK;
+}
+
+static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, const KsEpilogue& ep, int B,
+                           const KsWs& w, cudaStream_t s) {
     int r = ks_modup(c, in, level, B, w, s);
     if (r) return r;
-    {
-        const int by = B < 8 ? B : 8;
-        dim3 g(blocks_for(n / 2, 64), ne, (B + by - 1) / by);
-        ProfScope ps(PROF_INNER, 8.0 * n * ((double)B * nd * ne + 2.0 * nd * ne + 2.0 * B * ne), s);
-        k_ks_inner<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B,
-                                              c->t, nullptr, 0, nullptr, nullptr);
-        CHECK_KERNEL("ks inner");
-    }
+    r = key_inner_single(c, w, evk, B, level, nullptr, 0, s);
+    if (r) return r;
     return ks_moddown(c, level, ep, B, w, s);
 }
 
@@ -983,11 +997,6 @@ static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, in
 // by a warp-coalesced gather: a Galois permutation maps every 32-aligned run of
 // NTT slots onto a 32-aligned run), ONE ModDown; sum_t sigma_t(c0) is gathered
 // in the ModDown epilogue.
-struct HoistKeys {
-    int nsteps;
-    const u64* key[HELR_MAX_HOIST];
-    long long gal[HELR_MAX_HOIST];
-};
 // One thread per (coefficient i, extended limb e) carries the accumulators of
 // up to NB ciphertexts, so each key word is loaded once per launch chunk and
 // reused NB times from a register, and every step issues 2 nd + NB nd
@@ -1085,11 +1094,29 @@ __device__ __forceinline__ u128acc dresolve(const dacc& a) {  // hh 2^42 + mid 2
 
 // grid: x = coefficient tile * chunks + chunk (chunks of NB ciphertexts share
 // the tile's key words through L2 at the same time), y = extended limb e.
+// Kernel arguments of the key inner product (hoisted or single key).
+struct HoistArgs {
+    const u64* ext;
+    long long ext_item_stride, ext_digit_stride;
+    u64* acc;
+    long long acc_item_stride;
+    int n, log_n, nl, K, L, LK, B, nchunks, fold;
+    const u64* one_sh;
+    const u64* dadd;  // optional [B][3][L][N] tensor: Q limbs also get (P mod q) * (d0, d1)
+    long long dadd_is;
+    const u64* pm;
+    const u64* pm_sh;
+};
+
 template <int ND, int NB, bool DBL>
-__device__ __forceinline__ void hoist_body(const u64* __restrict__ ext, long long ext_item_stride,
-                                           long long ext_digit_stride, const HoistKeys& hk, u64* acc,
-                                           long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK,
-                                           int B, int nchunks, int fold, const Tables& tb, const u64* one_sh) {
+__device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs& A, const Tables& tb) {
+    const u64* __restrict__ ext = A.ext;
+    const long long ext_item_stride = A.ext_item_stride, ext_digit_stride = A.ext_digit_stride;
+    u64* acc = A.acc;
+    const long long acc_item_stride = A.acc_item_stride;
+    const int n = A.n, log_n = A.log_n, nl = A.nl, K = A.K, L = A.L, LK = A.LK, B = A.B, nchunks = A.nchunks,
+              fold = A.fold;
+    const u64* one_sh = A.one_sh;
     constexpr int W = (2 + NB) * ND;  // words per thread per stage
     constexpr int S = HOIST_STAGES;
     extern __shared__ u64 hsm[];
@@ -1196,30 +1223,34 @@ __device__ __forceinline__ void hoist_body(const u64* __restrict__ ext, long lon
     for (int b = 0; b < NB; b++) {
         if (b < nb) {
             u64* ap = acc + (size_t)(b0 + b) * acc_item_stride;
+            u64 o0, o1;
             if constexpr (DBL) {
-                ap[(size_t)e * n + i] = reduce128(dresolve(a0[b]), q, r1, r0, osh);
-                ap[((size_t)(nl + K) + e) * n + i] = reduce128(dresolve(a1[b]), q, r1, r0, osh);
+                o0 = reduce128(dresolve(a0[b]), q, r1, r0, osh);
+                o1 = reduce128(dresolve(a1[b]), q, r1, r0, osh);
             } else {
-                ap[(size_t)e * n + i] = reduce128(resolve(a0[b]), q, r1, r0, osh);
-                ap[((size_t)(nl + K) + e) * n + i] = reduce128(resolve(a1[b]), q, r1, r0, osh);
+                o0 = reduce128(resolve(a0[b]), q, r1, r0, osh);
+                o1 = reduce128(resolve(a1[b]), q, r1, r0, osh);
             }
+            if (A.dadd && e < nl) {  // merged ModDown + rescale: + (P mod q) * (d0, d1)
+                const u64* db = A.dadd + (size_t)(b0 + b) * A.dadd_is + (size_t)e * n + i;
+                const u64 w = A.pm[e], ws = A.pm_sh[e];
+                o0 = add_mod(o0, shoup(db[0], w, ws, q), q);
+                o1 = add_mod(o1, shoup(db[(size_t)L * n], w, ws, q), q);
+            }
+            ap[(size_t)e * n + i] = o0;
+            ap[((size_t)(nl + K) + e) * n + i] = o1;
         }
     }
 }
 
 template <int ND, int NB>
-__global__ void __launch_bounds__(HOIST_T, 3)
-k_ks_inner_hoisted(const u64* __restrict__ ext, long long ext_item_stride, long long ext_digit_stride, HoistKeys hk,
-                   u64* acc, long long acc_item_stride, int n, int log_n, int nl, int K, int L, int LK, int B,
-                   int nchunks, int fold, Tables tb, const u64* one_sh) {
+__global__ void __launch_bounds__(HOIST_T, 3) k_ks_inner_hoisted(HoistKeys hk, HoistArgs A, Tables tb) {
     const int e = blockIdx.y;
-    const int p = e < nl ? e : L + (e - nl);
+    const int p = e < A.nl ? e : A.L + (e - A.nl);
     if (tb.q[p] < NTT_DBL_BOUND)  // uniform per CTA (one limb per CTA)
-        hoist_body<ND, NB, true>(ext, ext_item_stride, ext_digit_stride, hk, acc, acc_item_stride, n, log_n, nl, K, L,
-                                 LK, B, nchunks, fold, tb, one_sh);
+        hoist_body<ND, NB, true>(hk, A, tb);
     else
-        hoist_body<ND, NB, false>(ext, ext_item_stride, ext_digit_stride, hk, acc, acc_item_stride, n, log_n, nl, K,
-                                  L, LK, B, nchunks, fold, tb, one_sh);
+        hoist_body<ND, NB, false>(hk, A, tb);
 }
 
 // Steps per 128-bit accumulation run: a run adds fold*nd products (each <
@@ -1237,20 +1268,16 @@ static int hoist_fold(const helr_ctx* c, int nd) {
 }
 
 template <int ND, int NB>
-static int launch_hoisted_nb(int nb, dim3 g, cudaStream_t s, const u64* ext, long long es, long long eds,
-                             const HoistKeys& hk, u64* acc, long long as, int n, int log_n, int nl, int K, int L,
-                             int LK, int fold, const Tables& tb, const u64* one_sh) {
-    const int nchunks = (nb + NB - 1) / NB;
+static void launch_hoisted_nb(dim3 g, cudaStream_t s, const HoistKeys& hk, HoistArgs A, const Tables& tb) {
+    A.nchunks = (A.B + NB - 1) / NB;
     const size_t smem = sizeof(u64) * (size_t)HOIST_STAGES * (2 + NB) * ND * HOIST_T;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_ks_inner_hoisted<ND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    g.x *= nchunks;
-    k_ks_inner_hoisted<ND, NB><<<g, HOIST_T, smem, s>>>(ext, es, eds, hk, acc, as, n, log_n, nl, K, L, LK, nb, nchunks,
-                                                        fold, tb, one_sh);
-    return 0;
+    g.x *= A.nchunks;
+    k_ks_inner_hoisted<ND, NB><<<g, HOIST_T, smem, s>>>(hk, A, tb);
 }
 // ciphertexts per thread: HELR_HOIST_NB (1, 2, 4 or 8; default 4) caps it
 static int hoist_nb_cap() {
@@ -1263,19 +1290,42 @@ static int hoist_nb_cap() {
     return cap;
 }
 template <int ND>
-static void launch_hoisted(int nb, dim3 g, cudaStream_t s, const u64* ext, long long es, long long eds,
-                           const HoistKeys& hk, u64* acc, long long as, int n, int log_n, int nl, int K, int L, int LK,
-                           int fold, const Tables& tb, const u64* one_sh) {
+static void launch_hoisted(dim3 g, cudaStream_t s, const HoistKeys& hk, const HoistArgs& A, const Tables& tb) {
+    const int nb = A.B;
     const int cap = hoist_nb_cap();
     const int want = nb <= 1 ? 1 : nb <= 2 ? 2 : nb <= 4 ? 4 : 8;
     const int NBs = want < cap ? want : cap;
-#define HELR_HNB(V) launch_hoisted_nb<ND, V>(nb, g, s, ext, es, eds, hk, acc, as, n, log_n, nl, K, L, LK, fold, tb, one_sh)
-    if (NBs == 1) HELR_HNB(1);
-    else if (NBs == 2) HELR_HNB(2);
-    else if (NBs == 4) HELR_HNB(4);
-    else if constexpr (ND <= 3) HELR_HNB(8);
-    else HELR_HNB(4);
-#undef HELR_HNB
+    if (NBs == 1) launch_hoisted_nb<ND, 1>(g, s, hk, A, tb);
+    else if (NBs == 2) launch_hoisted_nb<ND, 2>(g, s, hk, A, tb);
+    else if (NBs == 4) launch_hoisted_nb<ND, 4>(g, s, hk, A, tb);
+    else if constexpr (ND <= 3) launch_hoisted_nb<ND, 8>(g, s, hk, A, tb);
+    else launch_hoisted_nb<ND, 4>(g, s, hk, A, tb);
+}
+
+// Key inner product of the ModUp'd digits in w.ext with hk's keys (summed over
+// hk.nsteps Galois steps) into w.acc; dadd (optional) adds (P mod q)(d0, d1).
+static int key_inner(helr_ctx* c, const KsWs& w, const HoistKeys& hk, int nb, int level, const u64* dadd,
+                     long long dadd_is, cudaStream_t s) {
+    const int n = c->n, nl = level + 1, K = c->K, ne = nl + K;
+    const int nd = (nl + c->alpha - 1) / c->alpha;
+    dim3 g(blocks_for(n, HOIST_T), ne, 1);
+    HoistArgs A{w.ext, w.ext_s, w.ext_ds, w.acc, w.acc_s, n, c->log_n, nl, K, c->L, c->LK, nb, 1, hoist_fold(c, nd),
+                c->one_sh, dadd, dadd_is, c->pmod, c->pmod_sh};
+    ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne * hk.nsteps + 2.0 * nd * ne * hk.nsteps + 2.0 * nb * ne +
+                                        (dadd ? 2.0 * nb * nl : 0.0)), s);
+    switch (nd) {
+        case 1: launch_hoisted<1>(g, s, hk, A, c->t); break;
+        case 2: launch_hoisted<2>(g, s, hk, A, c->t); break;
+        case 3: launch_hoisted<3>(g, s, hk, A, c->t); break;
+        case 4: launch_hoisted<4>(g, s, hk, A, c->t); break;
+        case 5: launch_hoisted<5>(g, s, hk, A, c->t); break;
+        case 6: launch_hoisted<6>(g, s, hk, A, c->t); break;
+        case 7: launch_hoisted<7>(g, s, hk, A, c->t); break;
+        case 8: launch_hoisted<8>(g, s, hk, A, c->t); break;
+        default: set_error("key switching: more than 8 digits"); return HELR_EINVAL;
+    }
+    CHECK_KERNEL("key inner product");
+    return HELR_OK;
 }
 
 int op_rotsum_hoisted(helr_ctx* c, const u64* a, long long as, int nsteps, const long long* gal, const u64* const* keys,
@@ -1308,26 +1358,8 @@ int op_rotsum_hoisted(helr_ctx* c, const u64* a, long long as, int nsteps, const
         KsInput in{ab + (size_t)L * n, as, 0};
         int r = ks_modup(c, in, level, nb, w, s);
         if (r) return r;
-        {
-            dim3 g(blocks_for(n, HOIST_T), ne, 1);
-            const int fold = hoist_fold(c, nd);
-            ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne * nsteps + 2.0 * nd * ne * nsteps + 2.0 * nb * ne), s);
-#define HELR_HND(D) launch_hoisted<D>(nb, g, s, w.ext, w.ext_s, w.ext_ds, hk, w.acc, w.acc_s, n, c->log_n, nl, K, L, \
-                                     c->LK, fold, c->t, c->one_sh)
-            switch (nd) {
-                case 1: HELR_HND(1); break;
-                case 2: HELR_HND(2); break;
-                case 3: HELR_HND(3); break;
-                case 4: HELR_HND(4); break;
-                case 5: HELR_HND(5); break;
-                case 6: HELR_HND(6); break;
-                case 7: HELR_HND(7); break;
-                case 8: HELR_HND(8); break;
-                default: set_error("rotsum: more than 8 key-switching digits"); return HELR_EINVAL;
-            }
-#undef HELR_HND
-            CHECK_KERNEL("rotsum inner");
-        }
+        r = key_inner(c, w, hk, nb, level, nullptr, 0, s);
+        if (r) return r;
         KsEpilogue ep = make_epilogue(out + (size_t)b0 * os, os, include_identity ? ab : nullptr, as, ab, as, nsteps, gg);
         r = ks_moddown(c, level, ep, nb, w, s);
         if (r) return r;
@@ -1437,14 +1469,8 @@ int op_mul_relin_rescale_sum(helr_ctx* c, const u64* a, long long a_is, long lon
         KsInput in{w.tensor + 2ll * L * n, ts, 0};
         int r = ks_modup(c, in, level, nb, w, s);
         if (r) return r;
-        {
-            const int by = nb < 8 ? nb : 8;
-            dim3 g(blocks_for(n / 2, 64), ne, (nb + by - 1) / by);
-            ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne + 2.0 * nd * ne + 2.0 * nb * ne + 2.0 * nb * nl), s);
-            k_ks_inner<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, rlk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd,
-                                                  nb, c->t, w.tensor, ts, c->pmod, c->pmod_sh);
-            CHECK_KERNEL("ks inner (+Pd)");
-        }
+        r = key_inner_single(c, w, rlk, nb, level, w.tensor, ts, s);
+        if (r) return r;
         r = ks_moddown_rescale(c, level, out + (size_t)b0 * os, os, nb, w, s);
         if (r) return r;
     }
