@@ -623,11 +623,42 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
             }
         }
     }
+    // source residues as exact doubles (primes < 2^41) for the fp64 targets
+    double yd0[MA], yd1[MA];
+    bool ydok[MA];
+#pragma unroll
+    for (int k = 0; k < MA; k++) {
+        ydok[k] = k < ns && tb.q[lo + k] < NTT_DBL_BOUND;
+        if (ydok[k]) { yd0[k] = u2d(y0[k]); yd1[k] = u2d(y1[k]); }
+    }
     int t = 0;
     for (int e = 0; e < ne; e++) {
         if (e >= lo && e < hi) continue;
         const int p = e < a.nl ? e : a.L + (e - a.nl);
         const u64 q = tb.q[p];
+        if (q < NTT_DBL_BOUND) {
+            // fp64 target: exact signed products (mulmod_d), one reduction
+            const DblC dc{tb.qd[p], tb.qinvd[p]};
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < MA; k++) {
+                if (k < ns) {
+                    const u64 w = hm[(size_t)k * nt + t];
+                    if (ydok[k]) {
+                        const double wd = u2d(w);
+                        s0 = __dadd_rn(s0, mulmod_d(yd0[k], wd, dc));
+                        s1 = __dadd_rn(s1, mulmod_d(yd1[k], wd, dc));
+                    } else {  // wide source prime (q_0): integer Shoup, result < q
+                        const u64 ws = hms[(size_t)k * nt + t];
+                        s0 = __dadd_rn(s0, u2d(shoup(y0[k], w, ws, q)));
+                        s1 = __dadd_rn(s1, u2d(shoup(y1[k], w, ws, q)));
+                    }
+                }
+            }
+            st2(ext + (size_t)e * a.n + i, d2u_canon(s0, dc), d2u_canon(s1, dc));
+            t++;
+            continue;
+        }
         u64 s0 = 0, s1 = 0;
 #pragma unroll
         for (int k = 0; k < MA; k++) {
@@ -721,8 +752,34 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
     }
     const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
     const u64 rr1 = (u64)__double2ull_rd(__dadd_rn(v1, 0.5));
+    // sources as exact doubles when every special prime is below 2^41
+    bool dsrc = true;
+    double zd0[MK], zd1[MK];
+#pragma unroll
+    for (int k = 0; k < MK; k++) {
+        if (k < K) {
+            dsrc = dsrc && tb.q[L + k] < NTT_DBL_BOUND;
+            zd0[k] = u2d(z0[k] & 0x000FFFFFFFFFFFFFull);
+            zd1[k] = u2d(z1[k] & 0x000FFFFFFFFFFFFFull);
+        }
+    }
     for (int p = 0; p < nl; p++) {
         const u64 q = tb.q[p];
+        if (dsrc && q < NTT_DBL_BOUND) {  // fp64 target (see k_modup)
+            const DblC dc{tb.qd[p], tb.qinvd[p]};
+            const double pmd = u2d(pm[p]);
+            double s0 = -__dmul_rn(u2d(rr0), pmd), s1 = -__dmul_rn(u2d(rr1), pmd);  // exact: rr < K + 1
+#pragma unroll
+            for (int k = 0; k < MK; k++) {
+                if (k < K) {
+                    const double wd = u2d(phm[(size_t)k * L + p]);
+                    s0 = __dadd_rn(s0, mulmod_d(zd0[k], wd, dc));
+                    s1 = __dadd_rn(s1, mulmod_d(zd1[k], wd, dc));
+                }
+            }
+            st2(mp + (size_t)p * n + i, d2u_canon(s0, dc), d2u_canon(s1, dc));
+            continue;
+        }
         u64 s0 = 0, s1 = 0;
 #pragma unroll
         for (int k = 0; k < MK; k++) {
@@ -937,8 +994,33 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
     }
     const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
     const u64 rr1 = (u64)__double2ull_rd(__dadd_rn(v1, 0.5));
+    bool dsrc = true;
+    double zd0[MK], zd1[MK];
+#pragma unroll
+    for (int k = 0; k < MK; k++) {
+        if (k < ns) {
+            dsrc = dsrc && tb.q[k < K ? L + k : l] < NTT_DBL_BOUND;
+            zd0[k] = u2d(z0[k] & 0x000FFFFFFFFFFFFFull);
+            zd1[k] = u2d(z1[k] & 0x000FFFFFFFFFFFFFull);
+        }
+    }
     for (int p = 0; p < l; p++) {
         const u64 q = tb.q[p];
+        if (dsrc && q < NTT_DBL_BOUND) {  // fp64 target (see k_modup)
+            const DblC dc{tb.qd[p], tb.qinvd[p]};
+            const double mmd = u2d(mt.mm[p]);
+            double s0 = -__dmul_rn(u2d(rr0), mmd), s1 = -__dmul_rn(u2d(rr1), mmd);  // exact: rr <= K + 1
+#pragma unroll
+            for (int k = 0; k < MK; k++) {
+                if (k < ns) {
+                    const double wd = u2d(mt.hm[(size_t)k * L + p]);
+                    s0 = __dadd_rn(s0, mulmod_d(zd0[k], wd, dc));
+                    s1 = __dadd_rn(s1, mulmod_d(zd1[k], wd, dc));
+                }
+            }
+            st2(mp + (size_t)p * n + i, d2u_canon(s0, dc), d2u_canon(s1, dc));
+            continue;
+        }
         u64 s0 = 0, s1 = 0;
 #pragma unroll
         for (int k = 0; k < MK; k++) {
