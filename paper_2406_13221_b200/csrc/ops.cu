@@ -481,8 +481,20 @@ struct StCombine {
         const ulonglong2 xv = ld2(x + (size_t)item * x_is + (size_t)poly * x_ps + (size_t)p * n + off);
         ulonglong2 av = make_ulonglong2(0, 0);
         if (add_a) av = ld2(add_a + (size_t)item * a_is + (size_t)poly * a_ps + (size_t)p * n + off);
-        const u64 r0 = addends(shoup(sub_mod(xv.x, v.x, qq), wp, wps, qq), item, poly, p, off, qq, av.x);
-        const u64 r1 = addends(shoup(sub_mod(xv.y, v.y, qq), wp, wps, qq), item, poly, p, off + 1, qq, av.y);
+        u64 r0 = shoup(sub_mod(xv.x, v.x, qq), wp, wps, qq);
+        u64 r1 = shoup(sub_mod(xv.y, v.y, qq), wp, wps, qq);
+        if (add_a) { r0 = add_mod(r0, av.x, qq); r1 = add_mod(r1, av.y, qq); }
+        if (add_p && poly == 0) {
+            // off is even, and a Galois permutation maps the pair (off, off + 1)
+            // onto the aligned pair (s, s ^ 1): one index and one 16-byte load per step
+            const u64* pp = add_p + (size_t)item * p_is + (size_t)p * n;
+            for (int t = 0; t < ngal; t++) {
+                const int src = galois_perm(off, (u64)gal[t], log_n);
+                const ulonglong2 pr = ld2(pp + (src & ~1));
+                r0 = add_mod(r0, (src & 1) ? pr.y : pr.x, qq);
+                r1 = add_mod(r1, (src & 1) ? pr.x : pr.y, qq);
+            }
+        }
         st2(out + (size_t)item * out_is + (size_t)poly * out_ps + (size_t)p * n + off, r0, r1);
     }
 };
