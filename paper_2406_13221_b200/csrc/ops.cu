@@ -81,9 +81,16 @@ __global__ void k_elementwise(int op, const u64* a, const u64* b, u64* out, EwGe
             case EW_SUB: r = sub_mod(x, b[(size_t)item * g.bs + in_poly], q); break;
             case EW_ADDC: r = poly == 0 ? add_mod(x, b[limb], q) : x; break;
             case EW_ADDPT: r = poly == 0 ? add_mod(x, b[(size_t)limb * g.n + k], q) : x; break;
-            case EW_MULC: r = mul_mod(x, b[limb], q, tb.br1[limb], tb.br0[limb]); break;
-            case EW_MULPT: r = mul_mod(x, b[(size_t)limb * g.n + k], q, tb.br1[limb], tb.br0[limb]); break;
-            default: r = mul_mod(x, imul_f[(size_t)limb * g.n + k], q, tb.br1[limb], tb.br0[limb]); break;
+            default: {
+                const u64 y = op == EW_MULC ? b[limb] : (op == EW_MULPT ? b[(size_t)limb * g.n + k] : imul_f[(size_t)limb * g.n + k]);
+                if (q < NTT_DBL_BOUND) {
+                    const DblC dc{tb.qd[limb], tb.qinvd[limb]};
+                    r = d2u_canon(mulmod_d(u2d(x), u2d(y), dc), dc);
+                } else {
+                    r = mul_mod(x, y, q, tb.br1[limb], tb.br0[limb]);
+                }
+                break;
+            }
         }
         out[(size_t)item * g.os + in_poly] = r;
     }
@@ -418,8 +425,11 @@ __global__ void k_rescale_conv(const u64* r, u64* t, int n, int l, Tables tb) {
         const u64 v = r[(size_t)it * n + i];
         for (int p = 0; p < l; p++) {
             const u64 q = tb.q[p];
-            u64 w = v > half ? neg_mod((ql - v) % q, q) : v % q;
-            t[((size_t)it * l + p) * n + i] = w;
+            const u64 m = v > half ? ql - v : v;  // centred magnitude, < q_l
+            // q_l < 2q for every chain here (primes of similar size or q_0
+            // wider): one conditional subtraction instead of a 64-bit modulo
+            const u64 mr = ql <= 2 * q ? (m >= q ? m - q : m) : m % q;
+            t[((size_t)it * l + p) * n + i] = v > half ? neg_mod(mr, q) : mr;
         }
     }
 }
@@ -685,6 +695,78 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
     }
 }
 
+struct u128acc { u64 lo, hi; };
+// Split accumulator for a sum of 64x64-bit products: lo + hi 2^64 holds
+// sum x0 y0 + x1 y1 2^64, mid (+ carries 2^64) holds sum x0 y1 + x1 y0, so each
+// product costs four 32x32->64 multiply-adds with carry (aligned register
+// pairs, no shuffling) plus one carry count; resolved once per output.
+struct macc { u64 lo, hi, mid; u32 mc; };
+__device__ __forceinline__ void mac_split(macc& a, u64 x, u64 y) {
+    asm("{\n\t"
+        ".reg .u32 x0, x1, y0, y1, a0, a1, a2, a3, m0, m1;\n\t"
+        "mov.b64 {x0, x1}, %4;\n\t"
+        "mov.b64 {y0, y1}, %5;\n\t"
+        "mov.b64 {a0, a1}, %0;\n\t"
+        "mov.b64 {a2, a3}, %1;\n\t"
+        "mov.b64 {m0, m1}, %2;\n\t"
+        "mad.lo.cc.u32 a0, x0, y0, a0;\n\t"
+        "madc.hi.cc.u32 a1, x0, y0, a1;\n\t"
+        "madc.lo.cc.u32 a2, x1, y1, a2;\n\t"
+        "madc.hi.u32 a3, x1, y1, a3;\n\t"
+        "mad.lo.cc.u32 m0, x0, y1, m0;\n\t"
+        "madc.hi.cc.u32 m1, x0, y1, m1;\n\t"
+        "addc.u32 %3, %3, 0;\n\t"
+        "mad.lo.cc.u32 m0, x1, y0, m0;\n\t"
+        "madc.hi.cc.u32 m1, x1, y0, m1;\n\t"
+        "addc.u32 %3, %3, 0;\n\t"
+        "mov.b64 %0, {a0, a1};\n\t"
+        "mov.b64 %1, {a2, a3};\n\t"
+        "mov.b64 %2, {m0, m1};\n\t"
+        "}"
+        : "+l"(a.lo), "+l"(a.hi), "+l"(a.mid), "+r"(a.mc)
+        : "l"(x), "l"(y));
+}
+// lo + hi 2^64 + (mid + mc 2^64) 2^32 as a 128-bit value (< 2^128 by the fold bound)
+__device__ __forceinline__ u128acc resolve(const macc& a) {
+    u128acc r{a.lo, a.hi};
+    const u64 add_lo = a.mid << 32;
+    const u64 add_hi = (a.mid >> 32) | ((u64)a.mc << 32);
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r.lo), "+l"(r.hi) : "l"(add_lo), "l"(add_hi));
+    return r;
+}
+__device__ __forceinline__ u64 reduce128(const u128acc& a, u64 q, u64 r1, u64 r0, u64 one_sh) {
+    return barrett128(u128v{shoup(a.hi, 1, one_sh, q), a.lo}, q, r1, r0);
+}
+
+// fp64 multiply-accumulate for limbs whose prime is below 2^41: operands are
+// split at bit 21 into exact doubles (< 2^21), the four partial products
+// (< 2^42) accumulate exactly in three doubles for up to 2^11 terms (every
+// hoisted group has at most 31 * 8), and the sum is reassembled as a 128-bit
+// integer once per output.  DFMA issues at 2.5x the IMAD.WIDE rate on a pipe
+// the integer path leaves idle.
+struct dacc { double hh, mid, ll; };
+__device__ __forceinline__ void split21(u64 x, double& h, double& l) {
+    h = u2d(x >> 21);
+    l = u2d(x & 0x1FFFFFull);
+}
+__device__ __forceinline__ void mac_d(dacc& a, double xh, double xl, double yh, double yl) {
+    a.hh = __fma_rn(xh, yh, a.hh);
+    a.mid = __fma_rn(xh, yl, a.mid);
+    a.mid = __fma_rn(xl, yh, a.mid);
+    a.ll = __fma_rn(xl, yl, a.ll);
+}
+__device__ __forceinline__ u64 dexact(double x) {  // integer-valued 0 <= x < 2^52
+    return (u64)__double_as_longlong(__dadd_rn(x, NTT_TWO52)) & 0x000FFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ u128acc dresolve(const dacc& a) {  // hh 2^42 + mid 2^21 + ll
+    const u64 H = dexact(a.hh), M = dexact(a.mid), Lo = dexact(a.ll);
+    u128acc r{H << 42, H >> 22};
+    const u64 m_lo = M << 21, m_hi = M >> 43;
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r.lo), "+l"(r.hi) : "l"(m_lo), "l"(m_hi));
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(r.lo), "+l"(r.hi) : "l"(Lo));
+    return r;
+}
+
 // inner product: acc[b][poly][e] = sum_j ext[b][j][e] * evk[j][poly][prime(e)]
 // block (64, <= 8): threadIdx.y = ciphertext, so the 8 warps of a block read
 // the same key words (one DRAM read, L1 hits for the rest).
@@ -693,15 +775,37 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
 // rescale) yields rescale(d + KS(d2)).
 __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long ext_digit_stride, const u64* evk,
                            u64* acc, long long acc_item_stride, int n, int nl, int K, int L, int LK, int nd, int B,
-                           Tables tb, const u64* dadd, long long dadd_is, const u64* pm, const u64* pm_sh) {
+                           Tables tb, const u64* dadd, long long dadd_is, const u64* pm, const u64* pm_sh,
+                           const u64* one_sh) {
     const int e = blockIdx.y;
     const int b = blockIdx.z * blockDim.y + threadIdx.y;
     const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (b >= B || i >= n) return;
     const int p = e < nl ? e : L + (e - nl);
     const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
-    u128v a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
     const u64* xb = ext + (size_t)b * ext_item_stride + (size_t)e * n + i;
+    u64 o00, o01, o10, o11;
+    if (q < NTT_DBL_BOUND) {  // fp64 split-operand MACs (see hoist_body)
+        dacc c00{0.0, 0.0, 0.0}, c01{0.0, 0.0, 0.0}, c10{0.0, 0.0, 0.0}, c11{0.0, 0.0, 0.0};
+        for (int j = 0; j < nd; j++) {
+            const ulonglong2 k0 = ld2(evk + (((size_t)j * 2) * LK + p) * n + i);
+            const ulonglong2 k1 = ld2(evk + (((size_t)j * 2 + 1) * LK + p) * n + i);
+            const ulonglong2 u = ld2(xb + (size_t)j * ext_digit_stride);
+            double uxh, uxl, uyh, uyl, k0xh, k0xl, k0yh, k0yl, k1xh, k1xl, k1yh, k1yl;
+            split21(u.x, uxh, uxl); split21(u.y, uyh, uyl);
+            split21(k0.x, k0xh, k0xl); split21(k0.y, k0yh, k0yl);
+            split21(k1.x, k1xh, k1xl); split21(k1.y, k1yh, k1yl);
+            mac_d(c00, uxh, uxl, k0xh, k0xl);
+            mac_d(c01, uyh, uyl, k0yh, k0yl);
+            mac_d(c10, uxh, uxl, k1xh, k1xl);
+            mac_d(c11, uyh, uyl, k1yh, k1yl);
+        }
+        o00 = reduce128(dresolve(c00), q, r1, r0, one_sh[p]);
+        o01 = reduce128(dresolve(c01), q, r1, r0, one_sh[p]);
+        o10 = reduce128(dresolve(c10), q, r1, r0, one_sh[p]);
+        o11 = reduce128(dresolve(c11), q, r1, r0, one_sh[p]);
+    } else {
+    u128v a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
     for (int j = 0; j < nd; j++) {
         const ulonglong2 k0 = ld2(evk + (((size_t)j * 2) * LK + p) * n + i);
         const ulonglong2 k1 = ld2(evk + (((size_t)j * 2 + 1) * LK + p) * n + i);
@@ -717,9 +821,10 @@ __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long 
             a11 = u128v{0, barrett128(a11, q, r1, r0)};
         }
     }
+    o00 = barrett128(a00, q, r1, r0); o01 = barrett128(a01, q, r1, r0);
+    o10 = barrett128(a10, q, r1, r0); o11 = barrett128(a11, q, r1, r0);
+    }
     u64* ap = acc + (size_t)b * acc_item_stride;
-    u64 o00 = barrett128(a00, q, r1, r0), o01 = barrett128(a01, q, r1, r0);
-    u64 o10 = barrett128(a10, q, r1, r0), o11 = barrett128(a11, q, r1, r0);
     if (dadd && e < nl) {
         const u64* db = dadd + (size_t)b * dadd_is + (size_t)e * n + i;
         const ulonglong2 d0 = ld2(db), d1 = ld2(db + (size_t)L * n);
@@ -949,7 +1054,7 @@ static int key_inner_single(helr_ctx* c, const KsWs& w, const u64* evk, int B, i
     ProfScope ps(PROF_INNER, 8.0 * n * ((double)B * nd * ne + 2.0 * nd * ne + 2.0 * B * ne + (dadd ? 2.0 * B * nl : 0.0)),
                  s);
     k_ks_inner<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B,
-                                          c->t, dadd, dadd_is, c->pmod, c->pmod_sh);
+                                          c->t, dadd, dadd_is, c->pmod, c->pmod_sh, c->one_sh);
     CHECK_KERNEL("ks inner");
     return HELR_OK;
 }
@@ -1098,48 +1203,6 @@ static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, in
 // Accumulation is 128-bit: every product is < 2^122 (all primes < 2^61), so
 // up to 63 products fit; longer sums fold to a residue every `fold` steps
 // (host-computed from the largest prime, see hoist_fold).
-struct u128acc { u64 lo, hi; };
-// Split accumulator for a sum of 64x64-bit products: lo + hi 2^64 holds
-// sum x0 y0 + x1 y1 2^64, mid (+ carries 2^64) holds sum x0 y1 + x1 y0, so each
-// product costs four 32x32->64 multiply-adds with carry (aligned register
-// pairs, no shuffling) plus one carry count; resolved once per output.
-struct macc { u64 lo, hi, mid; u32 mc; };
-__device__ __forceinline__ void mac_split(macc& a, u64 x, u64 y) {
-    asm("{\n\t"
-        ".reg .u32 x0, x1, y0, y1, a0, a1, a2, a3, m0, m1;\n\t"
-        "mov.b64 {x0, x1}, %4;\n\t"
-        "mov.b64 {y0, y1}, %5;\n\t"
-        "mov.b64 {a0, a1}, %0;\n\t"
-        "mov.b64 {a2, a3}, %1;\n\t"
-        "mov.b64 {m0, m1}, %2;\n\t"
-        "mad.lo.cc.u32 a0, x0, y0, a0;\n\t"
-        "madc.hi.cc.u32 a1, x0, y0, a1;\n\t"
-        "madc.lo.cc.u32 a2, x1, y1, a2;\n\t"
-        "madc.hi.u32 a3, x1, y1, a3;\n\t"
-        "mad.lo.cc.u32 m0, x0, y1, m0;\n\t"
-        "madc.hi.cc.u32 m1, x0, y1, m1;\n\t"
-        "addc.u32 %3, %3, 0;\n\t"
-        "mad.lo.cc.u32 m0, x1, y0, m0;\n\t"
-        "madc.hi.cc.u32 m1, x1, y0, m1;\n\t"
-        "addc.u32 %3, %3, 0;\n\t"
-        "mov.b64 %0, {a0, a1};\n\t"
-        "mov.b64 %1, {a2, a3};\n\t"
-        "mov.b64 %2, {m0, m1};\n\t"
-        "}"
-        : "+l"(a.lo), "+l"(a.hi), "+l"(a.mid), "+r"(a.mc)
-        : "l"(x), "l"(y));
-}
-// lo + hi 2^64 + (mid + mc 2^64) 2^32 as a 128-bit value (< 2^128 by the fold bound)
-__device__ __forceinline__ u128acc resolve(const macc& a) {
-    u128acc r{a.lo, a.hi};
-    const u64 add_lo = a.mid << 32;
-    const u64 add_hi = (a.mid >> 32) | ((u64)a.mc << 32);
-    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r.lo), "+l"(r.hi) : "l"(add_lo), "l"(add_hi));
-    return r;
-}
-__device__ __forceinline__ u64 reduce128(const u128acc& a, u64 q, u64 r1, u64 r0, u64 one_sh) {
-    return barrett128(u128v{shoup(a.hi, 1, one_sh, q), a.lo}, q, r1, r0);
-}
 // Per-thread asynchronous prefetch: every thread copies the key words and
 // permuted ext words of rotation step t + S - 1 into its own shared-memory
 // slots (cp.async, 8 bytes each) while it multiplies step t, so the gathers'
@@ -1157,34 +1220,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int HOIST_T = 128;     // threads per block (coefficients per tile)
 constexpr int HOIST_STAGES = 3;  // steps in flight per thread
 
-// fp64 multiply-accumulate for limbs whose prime is below 2^41: operands are
-// split at bit 21 into exact doubles (< 2^21), the four partial products
-// (< 2^42) accumulate exactly in three doubles for up to 2^11 terms (every
-// hoisted group has at most 31 * 8), and the sum is reassembled as a 128-bit
-// integer once per output.  DFMA issues at 2.5x the IMAD.WIDE rate on a pipe
-// the integer path leaves idle.
-struct dacc { double hh, mid, ll; };
-__device__ __forceinline__ void split21(u64 x, double& h, double& l) {
-    h = u2d(x >> 21);
-    l = u2d(x & 0x1FFFFFull);
-}
-__device__ __forceinline__ void mac_d(dacc& a, double xh, double xl, double yh, double yl) {
-    a.hh = __fma_rn(xh, yh, a.hh);
-    a.mid = __fma_rn(xh, yl, a.mid);
-    a.mid = __fma_rn(xl, yh, a.mid);
-    a.ll = __fma_rn(xl, yl, a.ll);
-}
-__device__ __forceinline__ u64 dexact(double x) {  // integer-valued 0 <= x < 2^52
-    return (u64)__double_as_longlong(__dadd_rn(x, NTT_TWO52)) & 0x000FFFFFFFFFFFFFull;
-}
-__device__ __forceinline__ u128acc dresolve(const dacc& a) {  // hh 2^42 + mid 2^21 + ll
-    const u64 H = dexact(a.hh), M = dexact(a.mid), Lo = dexact(a.ll);
-    u128acc r{H << 42, H >> 22};
-    const u64 m_lo = M << 21, m_hi = M >> 43;
-    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r.lo), "+l"(r.hi) : "l"(m_lo), "l"(m_hi));
-    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(r.lo), "+l"(r.hi) : "l"(Lo));
-    return r;
-}
 
 // grid: x = coefficient tile * chunks + chunk (chunks of NB ciphertexts share
 // the tile's key words through L2 at the same time), y = extended limb e.
@@ -1484,6 +1519,25 @@ __global__ void k_tensor(TensorArgs ta, u64* d, int n, int L, Tables tb) {
     u64* d0 = d + (size_t)it * 3 * L * n + (size_t)p * n;
     u64* d1 = d0 + (size_t)L * n;
     u64* d2 = d1 + (size_t)L * n;
+    if (q < NTT_DBL_BOUND) {  // fp64 limb: exact signed products, one reduction (|sum| < 1.2 q * 2 terms)
+        const DblC dc{tb.qd[p], tb.qinvd[p]};
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+            for (int t = 0; t < ta.terms; t++) {
+                const u64* a0 = ta.a + (size_t)it * ta.a_is + (size_t)t * ta.a_ts + (size_t)p * n;
+                const u64* b0 = ta.b + (size_t)it * ta.b_is + (size_t)t * ta.b_ts + (size_t)p * n;
+                const double x0 = u2d(a0[i]), x1 = u2d(a0[(size_t)L * n + i]);
+                const double y0 = u2d(b0[i]), y1 = u2d(b0[(size_t)L * n + i]);
+                s0 = __dadd_rn(s0, mulmod_d(x0, y0, dc));
+                s1 = __dadd_rn(s1, __dadd_rn(mulmod_d(x0, y1, dc), mulmod_d(x1, y0, dc)));
+                s2 = __dadd_rn(s2, mulmod_d(x1, y1, dc));
+            }
+            d0[i] = d2u_canon(s0, dc);
+            d1[i] = d2u_canon(s1, dc);
+            d2[i] = d2u_canon(s2, dc);
+        }
+        return;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         u128v s0{0, 0}, s1{0, 0}, s2{0, 0};
         for (int t = 0; t < ta.terms; t++) {
