@@ -1,0 +1,264 @@
+// hoist.cu — key inner product for hoisted rotate-and-sums (and any batched
+// key switch): one thread per (coefficient, extended limb) carrying NB
+// ciphertexts, cp.async step prefetch, fp64 or 128-bit integer
+// multiply-accumulate.  Split from ops.cu so the two
+// translation units compile in parallel.
+#include <cstdlib>
+#include <type_traits>
+
+#include "ks.cuh"
+
+// Per-thread asynchronous prefetch: every thread copies the key words and
+// permuted ext words of rotation step t + S - 1 into its own shared-memory
+// slots (cp.async, 8 bytes each) while it multiplies step t, so the gathers'
+// latency overlaps the arithmetic without holding them in registers.  Each
+// slot is written and read by the same thread, so cp.async.wait_group alone
+// orders them (no block barrier).
+__device__ __forceinline__ void cp_async8(u64* dst, const u64* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int HOIST_T = 128;     // threads per block (coefficients per tile)
+constexpr int HOIST_STAGES = 3;  // steps in flight per thread
+
+
+// grid: x = coefficient tile * chunks + chunk (chunks of NB ciphertexts share
+// the tile's key words through L2 at the same time), y = extended limb e.
+// Kernel arguments of the key inner product (hoisted or single key).
+struct HoistArgs {
+    const u64* ext;
+    long long ext_item_stride, ext_digit_stride;
+    u64* acc;
+    long long acc_item_stride;
+    int n, log_n, nl, K, L, LK, B, nchunks, fold;
+    const u64* one_sh;
+    const u64* dadd;  // optional [B][3][L][N] tensor: Q limbs also get (P mod q) * (d0, d1)
+    long long dadd_is;
+    const u64* pm;
+    const u64* pm_sh;
+};
+
+template <int ND, int NB, bool DBL>
+__device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs& A, const Tables& tb) {
+    const u64* __restrict__ ext = A.ext;
+    const long long ext_item_stride = A.ext_item_stride, ext_digit_stride = A.ext_digit_stride;
+    u64* acc = A.acc;
+    const long long acc_item_stride = A.acc_item_stride;
+    const int n = A.n, log_n = A.log_n, nl = A.nl, K = A.K, L = A.L, LK = A.LK, B = A.B, nchunks = A.nchunks,
+              fold = A.fold;
+    const u64* one_sh = A.one_sh;
+    constexpr int W = (2 + NB) * ND;  // words per thread per stage
+    constexpr int S = HOIST_STAGES;
+    extern __shared__ u64 hsm[];
+    const int tid = threadIdx.x;
+    const int e = blockIdx.y;
+    const int tile = blockIdx.x / nchunks, chunk = blockIdx.x - tile * nchunks;
+    const int i = tile * HOIST_T + tid;
+    const int b0 = chunk * NB;
+    if (i >= n) return;
+    const int p = e < nl ? e : L + (e - nl);
+    const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p], osh = one_sh[p];
+    const int nb = B - b0 < NB ? B - b0 : NB;
+    const u64* xb = ext + (size_t)b0 * ext_item_stride + (size_t)e * n;
+    const size_t k0off = ((size_t)p) * n + i;
+    const size_t k1off = ((size_t)LK + p) * n + i;
+    const size_t kds = (size_t)2 * LK * n;
+    auto slot = [&](int stage, int w) -> u64* { return hsm + ((size_t)(stage * W + w) * HOIST_T + tid); };
+    auto issue = [&](int t) {
+        if (t < hk.nsteps) {
+            const int stage = t % S;
+            const int src = galois_perm(i, (u64)hk.gal[t], log_n);
+            const u64* kt = hk.key[t];
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                cp_async8(slot(stage, j), kt + (size_t)j * kds + k0off);
+                cp_async8(slot(stage, ND + j), kt + (size_t)j * kds + k1off);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                if (b < nb) {
+#pragma unroll
+                    for (int j = 0; j < ND; j++)
+                        cp_async8(slot(stage, 2 * ND + b * ND + j),
+                                  xb + (size_t)b * ext_item_stride + (size_t)j * ext_digit_stride + src);
+                }
+            }
+        }
+        cp_async_commit();  // empty groups keep the wait count uniform
+    };
+    using Acc = typename std::conditional<DBL, dacc, macc>::type;
+    Acc a0[NB], a1[NB];
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        if constexpr (DBL) a0[b] = a1[b] = dacc{0.0, 0.0, 0.0};
+        else a0[b] = a1[b] = macc{0, 0, 0, 0};
+    }
+#pragma unroll
+    for (int t = 0; t < S - 1; t++) issue(t);
+    int run = 0;
+    for (int t = 0; t < hk.nsteps; t++) {
+        issue(t + S - 1);
+        cp_async_wait<S - 1>();
+        const int stage = t % S;
+        if constexpr (DBL) {
+            double k0h[ND], k0l[ND], k1h[ND], k1l[ND];
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                split21(*slot(stage, j), k0h[j], k0l[j]);
+                split21(*slot(stage, ND + j), k1h[j], k1l[j]);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                if (b < nb) {
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        double uh, ul;
+                        split21(*slot(stage, 2 * ND + b * ND + j), uh, ul);
+                        mac_d(a0[b], uh, ul, k0h[j], k0l[j]);
+                        mac_d(a1[b], uh, ul, k1h[j], k1l[j]);
+                    }
+                }
+            }
+        } else {
+            if (run == fold) {  // fold into a residue before the 128-bit sum can overflow
+#pragma unroll
+                for (int b = 0; b < NB; b++) {
+                    a0[b] = macc{reduce128(resolve(a0[b]), q, r1, r0, osh), 0, 0, 0};
+                    a1[b] = macc{reduce128(resolve(a1[b]), q, r1, r0, osh), 0, 0, 0};
+                }
+                run = 0;
+            }
+            run++;
+            u64 k0[ND], k1[ND];
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                k0[j] = *slot(stage, j);
+                k1[j] = *slot(stage, ND + j);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                if (b < nb) {
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const u64 u = *slot(stage, 2 * ND + b * ND + j);
+                        mac_split(a0[b], u, k0[j]);
+                        mac_split(a1[b], u, k1[j]);
+                    }
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        if (b < nb) {
+            u64* ap = acc + (size_t)(b0 + b) * acc_item_stride;
+            u64 o0, o1;
+            if constexpr (DBL) {
+                o0 = reduce128(dresolve(a0[b]), q, r1, r0, osh);
+                o1 = reduce128(dresolve(a1[b]), q, r1, r0, osh);
+            } else {
+                o0 = reduce128(resolve(a0[b]), q, r1, r0, osh);
+                o1 = reduce128(resolve(a1[b]), q, r1, r0, osh);
+            }
+            if (A.dadd && e < nl) {  // merged ModDown + rescale: + (P mod q) * (d0, d1)
+                const u64* db = A.dadd + (size_t)(b0 + b) * A.dadd_is + (size_t)e * n + i;
+                const u64 w = A.pm[e], ws = A.pm_sh[e];
+                o0 = add_mod(o0, shoup(db[0], w, ws, q), q);
+                o1 = add_mod(o1, shoup(db[(size_t)L * n], w, ws, q), q);
+            }
+            ap[(size_t)e * n + i] = o0;
+            ap[((size_t)(nl + K) + e) * n + i] = o1;
+        }
+    }
+}
+
+template <int ND, int NB>
+__global__ void __launch_bounds__(HOIST_T, 3) k_ks_inner_hoisted(HoistKeys hk, HoistArgs A, Tables tb) {
+    const int e = blockIdx.y;
+    const int p = e < A.nl ? e : A.L + (e - A.nl);
+    if (tb.q[p] < NTT_DBL_BOUND)  // uniform per CTA (one limb per CTA)
+        hoist_body<ND, NB, true>(hk, A, tb);
+    else
+        hoist_body<ND, NB, false>(hk, A, tb);
+}
+
+// Steps per 128-bit accumulation run: a run adds fold*nd products (each <
+// 2^(2 bits)) to a residue (< 2^bits) and must stay below 2^128.
+static int hoist_fold(const helr_ctx* c, int nd) {
+    int bits = 0;
+    for (u64 q : c->primes) {
+        int b = 64 - __builtin_clzll(q);
+        if (b > bits) bits = b;
+    }
+    const int room = 128 - 2 * bits;  // 2^room products fit, less one for the residue
+    const long long terms = room >= 20 ? (1ll << 20) : (1ll << room) - 1;
+    const long long f = terms / nd;
+    return f < 1 ? 1 : (f > (1 << 20) ? (1 << 20) : (int)f);
+}
+
+template <int ND, int NB>
+static void launch_hoisted_nb(dim3 g, cudaStream_t s, const HoistKeys& hk, HoistArgs A, const Tables& tb) {
+    A.nchunks = (A.B + NB - 1) / NB;
+    const size_t smem = sizeof(u64) * (size_t)HOIST_STAGES * (2 + NB) * ND * HOIST_T;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ks_inner_hoisted<ND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    g.x *= A.nchunks;
+    k_ks_inner_hoisted<ND, NB><<<g, HOIST_T, smem, s>>>(hk, A, tb);
+}
+// ciphertexts per thread: HELR_HOIST_NB (1, 2, 4 or 8; default 4) caps it
+static int hoist_nb_cap() {
+    static int cap = -1;
+    if (cap < 0) {
+        const char* v = getenv("HELR_HOIST_NB");
+        cap = v ? atoi(v) : 4;
+        if (cap != 1 && cap != 2 && cap != 8) cap = 4;
+    }
+    return cap;
+}
+template <int ND>
+static void launch_hoisted(dim3 g, cudaStream_t s, const HoistKeys& hk, const HoistArgs& A, const Tables& tb) {
+    const int nb = A.B;
+    const int cap = hoist_nb_cap();
+    const int want = nb <= 1 ? 1 : nb <= 2 ? 2 : nb <= 4 ? 4 : 8;
+    const int NBs = want < cap ? want : cap;
+    if (NBs == 1) launch_hoisted_nb<ND, 1>(g, s, hk, A, tb);
+    else if (NBs == 2) launch_hoisted_nb<ND, 2>(g, s, hk, A, tb);
+    else if (NBs == 4) launch_hoisted_nb<ND, 4>(g, s, hk, A, tb);
+    else if constexpr (ND <= 3) launch_hoisted_nb<ND, 8>(g, s, hk, A, tb);
+    else launch_hoisted_nb<ND, 4>(g, s, hk, A, tb);
+}
+
+// Key inner product of the ModUp'd digits in w.ext with hk's keys (summed over
+// hk.nsteps Galois steps) into w.acc; dadd (optional) adds (P mod q)(d0, d1).
+int key_inner(helr_ctx* c, const KsWs& w, const HoistKeys& hk, int nb, int level, const u64* dadd,
+                     long long dadd_is, cudaStream_t s) {
+    const int n = c->n, nl = level + 1, K = c->K, ne = nl + K;
+    const int nd = (nl + c->alpha - 1) / c->alpha;
+    dim3 g(blocks_for(n, HOIST_T), ne, 1);
+    HoistArgs A{w.ext, w.ext_s, w.ext_ds, w.acc, w.acc_s, n, c->log_n, nl, K, c->L, c->LK, nb, 1, hoist_fold(c, nd),
+                c->one_sh, dadd, dadd_is, c->pmod, c->pmod_sh};
+    ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne * hk.nsteps + 2.0 * nd * ne * hk.nsteps + 2.0 * nb * ne +
+                                        (dadd ? 2.0 * nb * nl : 0.0)), s);
+    switch (nd) {
+        case 1: launch_hoisted<1>(g, s, hk, A, c->t); break;
+        case 2: launch_hoisted<2>(g, s, hk, A, c->t); break;
+        case 3: launch_hoisted<3>(g, s, hk, A, c->t); break;
+        case 4: launch_hoisted<4>(g, s, hk, A, c->t); break;
+        case 5: launch_hoisted<5>(g, s, hk, A, c->t); break;
+        case 6: launch_hoisted<6>(g, s, hk, A, c->t); break;
+        case 7: launch_hoisted<7>(g, s, hk, A, c->t); break;
+        case 8: launch_hoisted<8>(g, s, hk, A, c->t); break;
+        default: set_error("key switching: more than 8 digits"); return HELR_EINVAL;
+    }
+    CHECK_KERNEL("key inner product");
+    return HELR_OK;
+}
+
