@@ -48,6 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     cc = nvcc()
     extra = ["-Xptxas", "-v"] if os.environ.get("HELR_PTXAS_VERBOSE") else []
+    # experiment knobs, e.g. HELR_NVCC_DEFS="-DHELR_NTT_MINB=3"
+    extra += os.environ.get("HELR_NVCC_DEFS", "").split()
 
     def compile_one(src: Path) -> Path:
         obj = OBJ / (src.stem + ".o")

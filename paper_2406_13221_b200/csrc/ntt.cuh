@@ -411,7 +411,11 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
 }
 
 template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, class Ld, class St>
-__global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R), ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 256 ? 4 : 1)
+#ifndef HELR_NTT_MINB
+#define HELR_NTT_MINB 4  // resident 256-thread CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R),
+                                  ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 256 ? HELR_NTT_MINB : 1)
 ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     constexpr int T = 1 << LOG_T;
     __shared__ u64 sm[IS_COL ? T * (COLS + 1) : COLS * (T + T / 16)];
