@@ -34,6 +34,10 @@ struct NttPassArgs {
     int log_n;
     int st0;        // first global stage of this pass (forward numbering)
     int final_out;  // 1: reduce outputs to [0, q)
+    // fp64 limbs only: the intermediate buffer between the two passes of one
+    // transform holds raw doubles (integer-valued, |x| < 2^46) instead of
+    // canonical residues — saves the canonicalisation and the conversion back
+    int raw_in, raw_out;
 };
 
 template <int LOG_T, int LOG_R>
@@ -142,8 +146,9 @@ __device__ __forceinline__ void inv_last_h(int h, u64 (&x)[R], u64 ni, u64 nis, 
 // ---- fp64 path for primes < 2^41 ------------------------------------------
 // Residues of primes below 2^41 are exact doubles.  A twiddle product is
 // computed on the FP64 pipe (idle otherwise; DFMA issues at the IMAD rate,
-// 2.5x IMAD.WIDE): p = fl(a w), e = fma(a, w, -p) (exact), h = rint(p / q) by
-// the 1.5 2^52 trick, r = fma(-h, q, p) + e = a w - h q exactly, |r| < 0.6 q.
+// 2.5x IMAD.WIDE): p = fl(a w), e = fma(a, w, -p) (exact), h = rint(p / q) as
+// fma(p, 1/q, 1.5 2^52) - 1.5 2^52 (one rounding, to nearest), r = fma(-h, q,
+// p) + e = a w - h q exactly, |r| < 0.6 q: six fp64 instructions.
 // Signed values grow by < 0.6 q per forward stage and at most double per
 // inverse stage; a pass (<= 8 stages) starting from canonical inputs stays
 // below 2^50, so every intermediate is an exact integer-valued double, and
@@ -152,18 +157,26 @@ __device__ __forceinline__ void inv_last_h(int h, u64 (&x)[R], u64 ni, u64 nis, 
 constexpr double NTT_MAGIC = 6755399441055744.0;  // 1.5 * 2^52
 constexpr double NTT_TWO52 = 4503599627370496.0;  // 2^52
 struct DblC { double q, qinv; };
-__device__ __forceinline__ double drint(double x) { return __dsub_rn(__dadd_rn(x, NTT_MAGIC), NTT_MAGIC); }
+// rint(x * m) for |x * m| < 2^51: the fma rounds the exact product + 1.5 2^52
+// to an integer, the subtraction is exact
+__device__ __forceinline__ double drint_mul(double x, double m) {
+    return __dsub_rn(__fma_rn(x, m, NTT_MAGIC), NTT_MAGIC);
+}
 __device__ __forceinline__ double mulmod_d(double a, double w, const DblC& c) {
     const double p = __dmul_rn(a, w);
     const double e = __fma_rn(a, w, -p);
-    const double h = drint(__dmul_rn(p, c.qinv));
+    const double h = drint_mul(p, c.qinv);
     return __dadd_rn(__fma_rn(-h, c.q, p), e);
+}
+// integer-valued |x| < 2^50 -> x - rint(x / q) q, |result| <= q / 2 + 1 (exact)
+__device__ __forceinline__ double reduce_d(double x, const DblC& c) {
+    return __fma_rn(-drint_mul(x, c.qinv), c.q, x);
 }
 __device__ __forceinline__ double u2d(u64 x) {  // x < 2^52
     return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), NTT_TWO52);
 }
 __device__ __forceinline__ u64 d2u_canon(double x, const DblC& c) {  // integer-valued |x| < 2^50 -> [0, q)
-    double r = __fma_rn(-drint(__dmul_rn(x, c.qinv)), c.q, x);
+    double r = reduce_d(x, c);
     r = r < 0.0 ? __dadd_rn(r, c.q) : r;
     return (u64)__double_as_longlong(__dadd_rn(r, NTT_TWO52)) & 0x000FFFFFFFFFFFFFull;
 }
@@ -233,27 +246,35 @@ __device__ __forceinline__ void inv_last_dh(int h, double (&x)[R], double ni, do
     }
 }
 
+// Loaders / storers with kPtr expose the base address of limb li of item z
+// (plain strided buffers): the pass then addresses its elements as one
+// pointer plus compile-time offsets instead of a 64-bit product per element.
+template <class F, class = void>
+struct has_ptr { static constexpr bool value = false; };
+template <class F>
+struct has_ptr<F, decltype((void)F::kPtr)> { static constexpr bool value = F::kPtr; };
+
 // Primes below this bound take the fp64 path (uniform per CTA: one limb per CTA).
 constexpr u64 NTT_DBL_BOUND = 1ull << 41;
 
-template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, bool DBL, class Ld, class St>
+// (bx, li, z) = sub-transform tile, limb index in map, batch item.  S2 =
+// log N - LOG_T (column passes: the element stride is 2^S2, a compile-time
+// constant so every register's address is an immediate offset).
+template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, bool DBL, class Ld, class St>
 __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
-                                         const NttPassArgs& a, u64* sm) {
+                                         const NttPassArgs& a, u64* sm, const int bx, const int li, const int z) {
     using S = NttShape<LOG_T, LOG_R>;
     constexpr int T = S::T, R = S::R, NG = S::NG;
     constexpr int TPS = T / R;  // threads per sub-transform
     constexpr int SROW = IS_COL ? (COLS + 1) : (T + T / 16);
     using V = typename std::conditional<DBL, double, u64>::type;
 
-    const int li = blockIdx.y;
-    const int z = blockIdx.z;
     const int prime = map.prime[li];
     const u64 q = tb.q[prime];
     const u64 q2 = 4 * q;  // integer path: lazy half-range (see fwd_stage)
     DblC dc;
     if constexpr (DBL) dc = DblC{tb.qd[prime], tb.qinvd[prime]};
     const int n = 1 << a.log_n;
-    const int s2 = a.log_n - LOG_T;  // used by column passes
     const ulonglong2* W2 = reinterpret_cast<const ulonglong2*>(INV ? tb.itw : tb.tw) + (size_t)prime * n;
     const double* WD = (INV ? tb.itwd : tb.twd) + (size_t)prime * n;
 
@@ -261,18 +282,54 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
     int cc, s;
     if (IS_COL) { cc = tid % COLS; s = tid / COLS; }
     else { s = tid % TPS; cc = tid / TPS; }
-    const int sub = blockIdx.x * COLS + cc;  // global column / block index
+    const int sub = bx * COLS + cc;  // global column / block index
     const int sub_id = IS_COL ? 0 : sub;
     const int wrow = (1 << a.st0) + sub_id;  // twiddle index = (wrow << ls) + (k >> (qb + 1))
 
     auto goff = [&](int k) -> int {
-        return IS_COL ? (sub + (k << s2)) : ((sub << LOG_T) + k);
+        return IS_COL ? (sub + (k << S2)) : ((sub << LOG_T) + k);
+    };
+    // pointer fast path (kPtr functors): this thread's sub-transform base
+    // (lin / lout) and the CTA's contiguous tile base (row passes, lcta / scta)
+    constexpr bool LP = has_ptr<Ld>::value, SP = has_ptr<St>::value;
+    const u64* lin = nullptr;
+    const u64* lcta = nullptr;
+    u64* lout = nullptr;
+    u64* scta = nullptr;
+    if constexpr (LP) {
+        const u64* lb = ld.limb_ptr(z, li);
+        lin = lb + (IS_COL ? sub : (sub << LOG_T));
+        lcta = lb + ((bx * COLS) << LOG_T);
+    }
+    if constexpr (SP) {
+        u64* sb = st.limb_ptr(z, li);
+        lout = sb + (IS_COL ? sub : (sub << LOG_T));
+        scta = sb + ((bx * COLS) << LOG_T);
+    }
+    auto loff = [&](int k) -> int { return IS_COL ? (k << S2) : k; };
+    auto LD = [&](int k) -> u64 {
+        if constexpr (LP) return lin[loff(k)];
+        else return ld(z, li, prime, goff(k));
+    };
+    auto LD2 = [&](int k) -> ulonglong2 {
+        if constexpr (LP) return *reinterpret_cast<const ulonglong2*>(lin + loff(k));
+        else if constexpr (has_vec<Ld>::value) return ld.load2(z, li, prime, goff(k));
+        else return make_ulonglong2(0, 0);  // not reached: vector paths need kVec
+    };
+    auto ST = [&](int k, u64 v) {
+        if constexpr (SP) lout[loff(k)] = v;
+        else st(z, li, prime, goff(k), v);
+    };
+    auto ST2 = [&](int k, ulonglong2 v) {
+        if constexpr (SP) *reinterpret_cast<ulonglong2*>(lout + loff(k)) = v;
+        else if constexpr (has_vec<St>::value) st.store2(z, li, prime, goff(k), v);
     };
     auto sidx = [&](int k) -> int {
         return IS_COL ? (k * SROW + cc) : (cc * SROW + k + (k >> 4));
     };
+    const bool raw_in = DBL && a.raw_in;
     auto in_v = [&](u64 v) -> V {
-        if constexpr (DBL) return u2d(v);
+        if constexpr (DBL) return raw_in ? __longlong_as_double((long long)v) : u2d(v);
         else return v;
     };
     auto to_sm = [&](V v) -> u64 {
@@ -301,7 +358,9 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
 #pragma unroll 4
                     for (int e = 2 * tid; e < TOT; e += 2 * nthr) {
                         const int c2 = e >> LOG_T, k = e & (T - 1);
-                        const ulonglong2 v = ld.load2(z, li, prime, ((blockIdx.x * COLS + c2) << LOG_T) + k);
+                        ulonglong2 v;
+                        if constexpr (LP) v = *reinterpret_cast<const ulonglong2*>(lcta + e);
+                        else v = ld.load2(z, li, prime, ((bx * COLS + c2) << LOG_T) + k);
                         sm[c2 * SROW + k + (k >> 4)] = v.x;
                         sm[c2 * SROW + k + 1 + ((k + 1) >> 4)] = v.y;
                     }
@@ -311,23 +370,23 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                     __syncthreads();
                 } else {
 #pragma unroll
-                    for (int i = 0; i < R; i++) x[i] = in_v(ld(z, li, prime, goff(base + (i << lo))));
+                    for (int i = 0; i < R; i++) x[i] = in_v(LD(base + (i << lo)));
                 }
             } else if constexpr (!IS_COL && has_vec<Ld>::value) {
                 if (lo == 0) {
 #pragma unroll
                     for (int i = 0; i < R; i += 2) {
-                        const ulonglong2 v = ld.load2(z, li, prime, goff(base + i));
+                        const ulonglong2 v = LD2(base + i);
                         x[i] = in_v(v.x);
                         x[i + 1] = in_v(v.y);
                     }
                 } else {
 #pragma unroll
-                    for (int i = 0; i < R; i++) x[i] = in_v(ld(z, li, prime, goff(base + (i << lo))));
+                    for (int i = 0; i < R; i++) x[i] = in_v(LD(base + (i << lo)));
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < R; i++) x[i] = in_v(ld(z, li, prime, goff(base + (i << lo))));
+                for (int i = 0; i < R; i++) x[i] = in_v(LD(base + (i << lo)));
             }
         } else {
 #pragma unroll
@@ -366,7 +425,10 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
 #pragma unroll
             for (int i = 0; i < R; i++) {
                 if constexpr (DBL) {
-                    y[i] = d2u_canon(x[i], dc);  // every fp64 pass ends canonical
+                    if (a.raw_out)  // forward: |x| < 10 q; inverse: reduce the 2^8 growth
+                        y[i] = (u64)__double_as_longlong(INV ? reduce_d(x[i], dc) : x[i]);
+                    else
+                        y[i] = d2u_canon(x[i], dc);  // canonical [0, q)
                 } else {
                     u64 v = x[i];
                     if (a.final_out) {  // forward [0, 8q), inverse [0, 4q) -> [0, q)
@@ -388,19 +450,20 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                 for (int e = 2 * tid; e < TOT; e += 2 * nthr) {
                     const int c2 = e >> LOG_T, k = e & (T - 1);
                     const u64 v0 = sm[c2 * SROW + k + (k >> 4)], v1 = sm[c2 * SROW + k + 1 + ((k + 1) >> 4)];
-                    st.store2(z, li, prime, ((blockIdx.x * COLS + c2) << LOG_T) + k, make_ulonglong2(v0, v1));
+                    if constexpr (SP) *reinterpret_cast<ulonglong2*>(scta + e) = make_ulonglong2(v0, v1);
+                    else st.store2(z, li, prime, ((bx * COLS + c2) << LOG_T) + k, make_ulonglong2(v0, v1));
                 }
             } else if constexpr (!IS_COL && has_vec<St>::value) {
                 if (lo == 0) {
 #pragma unroll
-                    for (int i = 0; i < R; i += 2) st.store2(z, li, prime, goff(base + i), make_ulonglong2(y[i], y[i + 1]));
+                    for (int i = 0; i < R; i += 2) ST2(base + i, make_ulonglong2(y[i], y[i + 1]));
                 } else {
 #pragma unroll
-                    for (int i = 0; i < R; i++) st(z, li, prime, goff(base + (i << lo)), y[i]);
+                    for (int i = 0; i < R; i++) ST(base + (i << lo), y[i]);
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < R; i++) st(z, li, prime, goff(base + (i << lo)), y[i]);
+                for (int i = 0; i < R; i++) ST(base + (i << lo), y[i]);
             }
         } else {
 #pragma unroll
@@ -410,7 +473,7 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
     }
 }
 
-template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, class Ld, class St>
+template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, class Ld, class St>
 #ifndef HELR_NTT_MINB
 #define HELR_NTT_MINB 4  // resident 256-thread CTAs per SM the register budget is sized for
 #endif
@@ -420,9 +483,9 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     constexpr int T = 1 << LOG_T;
     __shared__ u64 sm[IS_COL ? T * (COLS + 1) : COLS * (T + T / 16)];
     if (tb.q[map.prime[blockIdx.y]] < NTT_DBL_BOUND)
-        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, true>(ld, st, tb, map, a, sm);
+        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true>(ld, st, tb, map, a, sm, blockIdx.x, blockIdx.y, blockIdx.z);
     else
-        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, false>(ld, st, tb, map, a, sm);
+        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, false>(ld, st, tb, map, a, sm, blockIdx.x, blockIdx.y, blockIdx.z);
 }
 
 // ---- plain functors: strided limb buffers -------------------------------
@@ -432,10 +495,14 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
 struct LdBuf {
     static constexpr bool kVec = true;
     static constexpr bool kTile = HELR_STBUF_TILE;
+    static constexpr bool kPtr = true;
     const u64* base;
     long long item_stride;
     LimbMap map;  // copy of the offsets (small)
     int n;
+    __device__ __forceinline__ const u64* limb_ptr(int z, int li) const {
+        return base + (size_t)z * item_stride + (size_t)map.off[li] * n;
+    }
     __device__ __forceinline__ u64 operator()(int z, int li, int, int off) const {
         return base[(size_t)z * item_stride + (size_t)map.off[li] * n + off];
     }
@@ -446,10 +513,14 @@ struct LdBuf {
 struct StBuf {
     static constexpr bool kVec = true;
     static constexpr bool kTile = HELR_STBUF_TILE;
+    static constexpr bool kPtr = true;
     u64* base;
     long long item_stride;
     LimbMap map;
     int n;
+    __device__ __forceinline__ u64* limb_ptr(int z, int li) const {
+        return base + (size_t)z * item_stride + (size_t)map.off[li] * n;
+    }
     __device__ __forceinline__ void operator()(int z, int li, int, int off, u64 v) const {
         base[(size_t)z * item_stride + (size_t)map.off[li] * n + off] = v;
     }
@@ -468,9 +539,10 @@ struct StBuf {
 // many SMs share the latency-bound work.
 constexpr long long NTT_SMALL_GRID = 2 * 148;
 
-template <int LOG_T, bool IS_COL, bool INV, class Ld, class St>
+template <int LOG_T, bool IS_COL, bool INV, int S2, class Ld, class St>
 static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
-                            int log_n, int st0, int final_out, int count, cudaStream_t s) {
+                            int log_n, int st0, int final_out, int count, cudaStream_t s, int raw_in = 0,
+                            int raw_out = 0) {
     constexpr int LOG_R = LOG_T < 4 ? LOG_T : 4;
     constexpr int T = 1 << LOG_T;
     // column passes: 16 adjacent columns (128-byte rows); row passes: ~4096 elements per CTA
@@ -479,21 +551,21 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
     constexpr int COLS_S = COLS >= 4 ? COLS / 4 : 1;
     const int subs = IS_COL ? (1 << (log_n - LOG_T)) : (1 << (log_n - LOG_T));
     const int cols = subs < COLS ? subs : COLS;  // tiny rings: fewer sub-transforms than COLS
-    NttPassArgs a{log_n, st0, final_out};
+    NttPassArgs a{log_n, st0, final_out, raw_in, raw_out};
     count_launches(1);
     if (cols == COLS) {
         const long long full = (long long)(subs / COLS) * map.count * count;
         if (COLS_S < COLS && full < NTT_SMALL_GRID && log_n >= 12) {
             dim3 grid(subs / COLS_S, map.count, count);
-            ntt_pass<LOG_T, LOG_R, COLS_S, IS_COL, INV><<<grid, T * COLS_S / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
+            ntt_pass<LOG_T, LOG_R, COLS_S, IS_COL, INV, S2><<<grid, T * COLS_S / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
             return;
         }
         dim3 grid(subs / COLS, map.count, count);
-        ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV><<<grid, T * COLS / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
+        ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV, S2><<<grid, T * COLS / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
     } else {
         // only reachable for single-pass rings (subs == 1)
         dim3 grid(subs / cols, map.count, count);
-        ntt_pass<LOG_T, LOG_R, 1, IS_COL, INV><<<grid, T / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
+        ntt_pass<LOG_T, LOG_R, 1, IS_COL, INV, S2><<<grid, T / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
     }
 }
 
@@ -501,7 +573,7 @@ template <bool INV, class Ld, class St>
 static void ntt_single(int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
                        int count, cudaStream_t s) {
     switch (log_n) {
-#define HELR_SP(LT) case LT: ntt_pass_launch<LT, false, INV>(ld, st, tb, map, log_n, 0, 1, count, s); break;
+#define HELR_SP(LT) case LT: ntt_pass_launch<LT, false, INV, 0>(ld, st, tb, map, log_n, 0, 1, count, s); break;
         HELR_SP(2) HELR_SP(3) HELR_SP(4) HELR_SP(5) HELR_SP(6) HELR_SP(7) HELR_SP(8) HELR_SP(9)
         HELR_SP(10) HELR_SP(11)
 #undef HELR_SP
@@ -511,10 +583,16 @@ static void ntt_single(int log_n, const Ld& ld, const St& st, const Tables& tb, 
 
 template <bool INV, class Ld, class St>
 static void ntt_col(int lt, int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
-                    int final_out, int count, cudaStream_t s) {
-    switch (lt) {
-#define HELR_CP(LT) case LT: ntt_pass_launch<LT, true, INV>(ld, st, tb, map, log_n, 0, final_out, count, s); break;
-        HELR_CP(6) HELR_CP(7) HELR_CP(8)
+                    int final_out, int count, cudaStream_t s, int raw_in, int raw_out) {
+    // column pass of log N = LN: LT = floor(LN / 2) stages (= lt), element stride 2^(LN - LT)
+    (void)lt;
+    switch (log_n) {
+#define HELR_CP(LN) \
+    case LN: \
+        ntt_pass_launch<(LN) / 2, true, INV, (LN) - (LN) / 2>(ld, st, tb, map, log_n, 0, final_out, count, s, raw_in, \
+                                                              raw_out); \
+        break;
+        HELR_CP(12) HELR_CP(13) HELR_CP(14) HELR_CP(15) HELR_CP(16)
 #undef HELR_CP
         default: break;
     }
@@ -522,10 +600,11 @@ static void ntt_col(int lt, int log_n, const Ld& ld, const St& st, const Tables&
 
 template <bool INV, class Ld, class St>
 static void ntt_row(int lt, int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
-                    int final_out, int count, cudaStream_t s) {
+                    int final_out, int count, cudaStream_t s, int raw_in, int raw_out) {
     const int st0 = log_n - lt;
     switch (lt) {
-#define HELR_RP(LT) case LT: ntt_pass_launch<LT, false, INV>(ld, st, tb, map, log_n, st0, final_out, count, s); break;
+#define HELR_RP(LT) \
+    case LT: ntt_pass_launch<LT, false, INV, 0>(ld, st, tb, map, log_n, st0, final_out, count, s, raw_in, raw_out); break;
         HELR_RP(6) HELR_RP(7) HELR_RP(8) HELR_RP(9)
 #undef HELR_RP
         default: break;
@@ -547,11 +626,11 @@ static void ntt_launch(const helr_ctx* c, const Ld& ld, const St& st, u64* mid, 
     StBuf smid{mid, mid_stride, map, c->n};
     LdBuf lmid{mid, mid_stride, map, c->n};
     if (!INV) {
-        ntt_col<false>(s1, log_n, ld, smid, c->t, map, 0, count, s);
-        ntt_row<false>(s2, log_n, lmid, st, c->t, map, 1, count, s);
+        ntt_col<false>(s1, log_n, ld, smid, c->t, map, 0, count, s, 0, 1);
+        ntt_row<false>(s2, log_n, lmid, st, c->t, map, 1, count, s, 1, 0);
     } else {
-        ntt_row<true>(s2, log_n, ld, smid, c->t, map, 0, count, s);
-        ntt_col<true>(s1, log_n, lmid, st, c->t, map, 1, count, s);
+        ntt_row<true>(s2, log_n, ld, smid, c->t, map, 0, count, s, 0, 1);
+        ntt_col<true>(s1, log_n, lmid, st, c->t, map, 1, count, s, 1, 0);
     }
 }
 
