@@ -247,8 +247,17 @@ def main():
     ck = CkksParams.generate(log_n=wl["log_n"], n_q=wl["L"], dnum=args.dnum or wl["dnum"])
     ctx = GpuContext(ck, seed=1, max_batch=max(8, wl["blocks"]))
     ds = make_dataset(wl["data"])
+    # full batch on N > 1 GPUs: the ranks share each iteration's batches and
+    # all-reduce the gradient residues (shard.py; strong scaling); the
+    # mini-batch path does not shard, so N GPUs run N replicas (weak scaling)
+    sharded = ws > 1 and wl["mode"] == "full_batch"
+    shard_kw = {}
+    if sharded:
+        from paper_2406_13221_b200.shard import ResidueAllReduce
+        shard_kw = dict(shard=(rank, ws), reducer=ResidueAllReduce(tuple(ck.q) + tuple(ck.p)))
     tr = FusedTrainer(ctx, ds, rows_per_block=wl["rows"], blocks_per_batch=wl["blocks"], mode=wl["mode"],
-                      use_graph=not args.no_graph, bsgs_bits=args.bsgs_bits, rows_bits=args.rows_bits)
+                      use_graph=not args.no_graph, bsgs_bits=args.bsgs_bits, rows_bits=args.rows_bits, **shard_kw)
+    job = (lambda n, w, m: n / (m / 1000.0)) if sharded else job_throughput
     setup_s = time.perf_counter() - t_setup
     steps = args.steps if args.steps is not None else tr.n_batches
     warm = max(3, args.warmup)
@@ -275,7 +284,7 @@ def main():
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1), ws)
-    value = job_throughput(steps, ws, ms)
+    value = job(steps, ws, ms)
 
     # ---------------- live per-kernel attribution: CUDA events recorded inside a
     # captured graph (no host launch gaps), one category pair per launch
@@ -326,7 +335,7 @@ def main():
         barrier()
         ems = max_over_ranks(f0.elapsed_time(f1), ws)
         h2d, d2h = tr.bytes_per_step()
-        e2e = {"value": job_throughput(steps, ws, ems), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": job(steps, ws, ems), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / steps}
         tr.disable_host_stream()
 
@@ -340,15 +349,17 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps, "warmup": warm,
-            "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None,
             "dtype": "u64", "data": "synthetic",
             "config": {"workload": args.workload, "n": ds.n_samples, "features": ds.n_features,
                        "padded_cols": tr.layout.col_blocks * tr.layout.g, "log_n": ck.log_n, "L": ck.L,
                        "K": ck.K, "dnum": ck.dnum, "batch_rows": tr.batch_rows, "cts_per_batch": tr.rows,
-                       "batches": tr.n_batches, "mode": wl["mode"], "parallelism": "replicas",
+                       "batches": tr.n_batches, "mode": wl["mode"],
+                       "parallelism": f"shard{ws}" if sharded else "replicas",
                        "cuda_graph": tr.use_graph, "rotsum_group_bits": tr.log_baby, "rows_group_bits": tr.log_baby_rows,
                        "l2": "no flush needed: each step streams a new 64 MiB batch and ~2 GB of keys"},
-            "epoch_s": tr.n_batches / (value / ws),
+            "epoch_s": (1.0 / value) if wl["mode"] == "full_batch" else tr.n_batches / (value / ws),
             "hbm_gbs_step": step_gb / (ms / steps / 1000.0),
             "algorithmic_gb_per_step": step_gb,
             "roofline": roofline,

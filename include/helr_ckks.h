@@ -114,6 +114,11 @@ int helr_add_plain(helr_ctx* ctx, const uint64_t* a, const uint64_t* pt,
 int helr_mul_const(helr_ctx* ctx, const uint64_t* a, const uint64_t* c,
                    uint64_t* out, int count, int level, void* stream);
 /* Both polynomials times an NTT plaintext; no rescale. */
+/* Fold every residue word (any value < 2^64, e.g. the element-wise sum of up
+ * to 8 ranks' residue vectors after an all-reduce) back to [0, q_i).  New:
+ * the combine step of the sharded full-batch gradient; the
+ * reference sums block gradients with SimContext.add (enctrain.py:374-381). */
+int helr_reduce(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count, int level, void* stream);
 int helr_mul_plain(helr_ctx* ctx, const uint64_t* a, const uint64_t* pt,
                    uint64_t* out, int count, int level, void* stream);
 /* Drop q_level: out (level-1) = round(in / q_level). */

@@ -48,6 +48,7 @@ SIGNATURES = {
     "helr_add_plain": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_const": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_plain": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],
+    "helr_reduce": [_vp, _u64p, _u64p, _i, _i, _vp],
     "helr_rescale": [_vp, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_relin": [_vp, _u64p, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_relin_rescale": [_vp, _u64p, _u64p, _u64p, _u64p, _i, _i, _vp],

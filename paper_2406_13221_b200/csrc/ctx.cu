@@ -317,6 +317,7 @@ extern "C" int helr_ctx_destroy(helr_ctx* c) {
     cudaFree(c->d_tab);
     cudaFree(c->d_modup_offs);
     cudaFree(c->ws);
+    cudaFree(c->nag_ws);
     delete c;
     return HELR_OK;
 }

@@ -71,6 +71,9 @@ struct helr_ctx {
     // key-switching workspace
     u64* ws = nullptr;
     size_t ws_words = 0;
+    // fused-iteration driver workspace (nag.cu), allocated on first use
+    u64* nag_ws = nullptr;
+    size_t nag_words = 0;
 };
 
 void set_error(const std::string& msg);

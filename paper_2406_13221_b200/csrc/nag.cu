@@ -25,27 +25,21 @@
         if (_r) return _r;     \
     } while (0)
 
-struct NagBuffers {
-    int rows = 0, cols = 0;
-    u64* base = nullptr;
-    size_t words = 0;
-};
-
-static NagBuffers g_nb;  // one driver workspace per process (single stream use)
-
+// The driver workspace belongs to the context (like the key-switching
+// workspace): contexts used from different streams never share scratch.
 static int nag_buffers(helr_ctx* c, int rows, int cols, u64** out) {
     const size_t cs = 2ull * c->L * c->n;
     const size_t need = cs * (7ull * rows + 5ull * cols);
-    if (g_nb.base && g_nb.words >= need) { *out = g_nb.base; return HELR_OK; }
-    if (g_nb.base) { cudaFree(g_nb.base); g_nb.base = nullptr; }
+    if (c->nag_ws && c->nag_words >= need) { *out = c->nag_ws; return HELR_OK; }
     cudaStreamCaptureStatus st;
     if (cudaStreamIsCapturing(0, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
         set_error("nag workspace must be allocated before graph capture (run one iteration first)");
         return HELR_EINVAL;
     }
-    if (!cuda_ok(cudaMalloc(&g_nb.base, need * sizeof(u64)), "cudaMalloc(nag workspace)")) return HELR_ENOMEM;
-    g_nb.words = need;
-    *out = g_nb.base;
+    if (c->nag_ws) { cudaFree(c->nag_ws); c->nag_ws = nullptr; c->nag_words = 0; }
+    if (!cuda_ok(cudaMalloc(&c->nag_ws, need * sizeof(u64)), "cudaMalloc(nag workspace)")) return HELR_ENOMEM;
+    c->nag_words = need;
+    *out = c->nag_ws;
     return HELR_OK;
 }
 

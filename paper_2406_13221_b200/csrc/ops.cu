@@ -53,6 +53,7 @@ __global__ void k_elementwise(int op, const u64* a, const u64* b, u64* out, EwGe
             case EW_SUB: r = sub_mod(x, b[(size_t)item * g.bs + in_poly], q); break;
             case EW_ADDC: r = poly == 0 ? add_mod(x, b[limb], q) : x; break;
             case EW_ADDPT: r = poly == 0 ? add_mod(x, b[(size_t)limb * g.n + k], q) : x; break;
+            case EW_REDUCE: r = barrett128(u128v{0, x}, q, tb.br1[limb], tb.br0[limb]); break;
             default: {
                 const u64 y = op == EW_MULC ? b[limb] : (op == EW_MULPT ? b[(size_t)limb * g.n + k] : imul_f[(size_t)limb * g.n + k]);
                 if (q < NTT_DBL_BOUND) {
@@ -77,6 +78,7 @@ int op_ew(helr_ctx* c, int op, const u64* a, long long as, const u64* b, long lo
     int blocks = blocks_for(total, 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     ProfScope ps(PROF_ELEM, 8.0 * total * ((op == EW_ADD || op == EW_SUB) ? 3 : 2), s);
+    if (op == EW_REDUCE) b = a;  // unary
     k_elementwise<<<blocks, 256, 0, s>>>(op, a, b, out, g, total, c->t, c->imul_f);
     CHECK_KERNEL("elementwise");
     return HELR_OK;
@@ -106,6 +108,10 @@ extern "C" int helr_add_plain(helr_ctx* c, const uint64_t* a, const uint64_t* pt
 extern "C" int helr_mul_const(helr_ctx* c, const uint64_t* a, const uint64_t* k, uint64_t* out, int count, int level, void* s) {
     clear_stale_error("helr_mul_const");
     return launch_ew(c, EW_MULC, (const u64*)a, (const u64*)k, (u64*)out, count, level, s);
+}
+extern "C" int helr_reduce(helr_ctx* c, const uint64_t* a, uint64_t* out, int count, int level, void* s) {
+    clear_stale_error("helr_reduce");
+    return launch_ew(c, EW_REDUCE, (const u64*)a, nullptr, (u64*)out, count, level, s);
 }
 extern "C" int helr_mul_plain(helr_ctx* c, const uint64_t* a, const uint64_t* pt, uint64_t* out, int count, int level, void* s) {
     clear_stale_error("helr_mul_plain");

@@ -8,7 +8,7 @@
 #define HELR_MAX_HOIST 32
 #include "ctx.cuh"
 
-enum EwOp { EW_ADD = 0, EW_SUB, EW_ADDC, EW_ADDPT, EW_MULC, EW_MULPT, EW_IMUL };
+enum EwOp { EW_ADD = 0, EW_SUB, EW_ADDC, EW_ADDPT, EW_MULC, EW_MULPT, EW_IMUL, EW_REDUCE };
 
 int op_ew(helr_ctx* c, int op, const u64* a, long long as, const u64* b, long long bs, u64* out, long long os,
           int count, int level, cudaStream_t s);

@@ -32,6 +32,7 @@ from . import _lib
 from .ckks import GpuContext
 from .encoding import BlockLayout, pack_matrix_array, plan_layout, replicate_rows
 from .optimizer import ALPHA0_INIT, BASELINE_CUBIC, PolyApprox, lr_at, merge_bbar, next_alpha, scaler_for
+from .shard import partition
 
 __all__ = ["IterPlan", "plan_iteration", "NagArgs", "FusedTrainer", "NCONST", "ITER_DEPTH"]
 
@@ -179,7 +180,8 @@ class FusedTrainer:
     def __init__(self, ctx: GpuContext, ds, rows_per_block: int, blocks_per_batch: int = 1,
                  mode: str = "mini_batch", poly: PolyApprox = BASELINE_CUBIC, schedule=None,
                  epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False, bsgs: bool = True,
-                 refresh_bits: int = 47, bsgs_bits: Optional[int] = None, rows_bits: Optional[int] = None):
+                 refresh_bits: int = 47, bsgs_bits: Optional[int] = None, rows_bits: Optional[int] = None,
+                 shard: tuple = (0, 1), reducer=None):
         if mode not in ("mini_batch", "full_batch"):
             raise ValueError(f"mode must be mini_batch or full_batch, got {mode!r}")
         from .optimizer import ExpDecay
@@ -192,6 +194,14 @@ class FusedTrainer:
         self.epsilon = epsilon
         self.enhanced = enhanced
         self.use_graph = use_graph
+        # full-batch sharding (shard.py): this rank's batches, and the in-place
+        # SUM of the raw gradient residues across ranks (None: single rank)
+        self.shard_rank, self.shard_world = int(shard[0]), int(shard[1])
+        if self.shard_world > 1 and mode != "full_batch":
+            raise ValueError("only the full-batch gradient shards; mini-batch runs replicas")
+        if self.shard_world > 1 and reducer is None:
+            raise ValueError("a sharded trainer needs a reducer (shard.ResidueAllReduce)")
+        self.reducer = reducer
         # W, V re-enter each iteration at scale 2^refresh_bits: above Delta = 2^40
         # so the refresh's fresh encryption noise is negligible, below 2^50 so
         # the row-start mask still encodes at >= 2^35
@@ -508,11 +518,18 @@ class FusedTrainer:
             if self.host_stream:
                 self._release((b + 1) % nbt, (b + 1) % nbt)
         else:
-            for bb in range(nbt):
-                zb = self._stage(bb, 0, with_bbar=(bb == 0))
-                self._run(self._args(plan, 1 if bb == 0 else 2, zb))
+            mine = partition(nbt, self.shard_rank, self.shard_world)
+            zb = None
+            for i, bb in enumerate(mine):
+                zb = self._stage(bb, 0, with_bbar=(i == 0))
+                self._run(self._args(plan, 1 if i == 0 else 2, zb))
                 if self.host_stream:
-                    self._release((bb + 1) % nbt, 0)
+                    self._release(mine[(i + 1) % len(mine)], 0)
+            if zb is None:  # more ranks than batches: this rank contributes zero
+                self.grad.zero_()
+                zb = self._stage(0, 0)
+            if self.shard_world > 1:
+                self.combine_gradient()
             self._run(self._args(plan, 3, zb))
             if self.host_stream:  # the finish phase reads the last buffer's B̄ too
                 ev = torch.cuda.Event()
@@ -529,6 +546,14 @@ class FusedTrainer:
             self.w_host[:, :, :lv].copy_(self.wv[:, :, :lv], non_blocking=True)
         return dict(iteration=self.t, lr=lr, eta=eta, gamma=gamma, level_start=level_start,
                     level_after=self.level, refreshed=refreshed)
+
+    def combine_gradient(self):
+        """Sum the ranks' partial gradients (raw residue words, exact in 63
+        bits) and fold them back to canonical residues on the device."""
+        self.reducer(self.grad)
+        lv = self.level - 5  # the gradient's level (helr_nag_args.grad)
+        self.ctx._call("helr_reduce", self.grad.data_ptr(), self.grad.data_ptr(), self.cols, lv,
+                       torch.cuda.current_stream().cuda_stream)
 
     # ------------------------------------------------------------ readout
     def weights(self) -> np.ndarray:

@@ -78,3 +78,65 @@ def test_reference_arm_under_torchrun_two_ranks():
     assert line["impl"] == "reference" and line["n_gpus"] == 2
     assert line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] in ("port", "reference")
+
+
+# ---- sharded full-batch gradient: host logic over gloo -------------------
+def test_partition_covers_every_batch_once():
+    sys.path.insert(0, str(ROOT))
+    from paper_2406_13221_b200.shard import partition
+    for nb in (0, 1, 5, 413):
+        for ws in (1, 2, 3, 8):
+            parts = [partition(nb, r, ws) for r in range(ws)]
+            flat = sorted(b for p in parts for b in p)
+            assert flat == list(range(nb))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        partition(4, 2, 2)
+
+
+def test_max_world_bound():
+    sys.path.insert(0, str(ROOT))
+    from paper_2406_13221_b200.params import CkksParams
+    from paper_2406_13221_b200.shard import max_world
+    ck = CkksParams.generate(log_n=13, n_q=8, dnum=2)
+    assert max_world(ck.q + ck.p) >= 8  # q_0 < 2^60: eight 60-bit residues fit in 63 bits
+    assert max_world([(1 << 62) - 57]) == 2 and max_world([(1 << 62) + 135]) == 1
+
+
+def _residue_worker(rank, ws, port, q, out):
+    sys.path.insert(0, str(ROOT))
+    import numpy as np
+    from paper_2406_13221_b200.shard import ResidueAllReduce
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        rng = np.random.default_rng(100 + rank)
+        mine = rng.integers(0, np.array(q, dtype=np.uint64)[:, None], size=(len(q), 64), dtype=np.uint64)
+        t = torch.from_numpy(mine.view(np.int64).copy())
+        ResidueAllReduce(q)(t)
+        out.put((rank, mine, t.numpy().view(np.uint64).copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_residue_allreduce_gloo_is_exact():
+    """Two ranks' residue words summed by the all-reduce reduce mod q to the
+    sum of the residues mod q (what helr_reduce then computes on the GPU)."""
+    import numpy as np
+    qs = [(1 << 60) - 93, (1 << 40) + 1281, (1 << 40) - 87]
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_residue_worker, args=(r, 2, port, qs, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((out.get(timeout=120) for _ in procs), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    qv = np.array(qs, dtype=np.uint64)[:, None]
+    want = (res[0][1] % qv + res[1][1] % qv) % qv
+    for _, _, summed in res:
+        assert np.all(summed < (1 << 63))
+        np.testing.assert_array_equal(summed % qv, want)

@@ -40,16 +40,23 @@ def main():
     for p in range(L):
         data[:, p].copy_(torch.randint(0, int(ck.q[p]), (B, n), device="cuda", generator=g, dtype=torch.int64))
     st = torch.cuda.current_stream().cuda_stream
-    if a.once:
+    if a.once:  # profiled region only (ncu --profile-from-start off)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
         _lib.call("helr_ntt_fwd", ctx.handle, data.data_ptr() + 8 * n, 1, L - 1, B, L * n, st)
         _lib.call("helr_ntt_inv", ctx.handle, data.data_ptr() + 8 * n, 1, L - 1, B, L * n, st)
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         return
     ref = data.clone()
     out = {}
-    for name, first, cnt in (("fp64", 1, L - 1), ("int_q0", 0, 1)):
+    big = torch.empty((8 * B, 1, n), dtype=torch.int64, device="cuda")  # q_0 only, 8x the items
+    big.copy_(torch.randint(0, int(ck.q[0]), (8 * B, 1, n), device="cuda", generator=g, dtype=torch.int64))
+    for name, first, cnt in (("fp64", 1, L - 1), ("int_q0", 0, 1), ("mixed", 0, L), ("int_q0_big", 0, 1)):
+        buf, items, stride = (big, 8 * B, n) if name == "int_q0_big" else (data, B, L * n)
         for d in ("fwd", "inv"):
-            fn = lambda: _lib.call(f"helr_ntt_{d}", ctx.handle, data.data_ptr() + 8 * n * first, first, cnt, B, L * n, st)
+            fn = lambda: _lib.call(f"helr_ntt_{d}", ctx.handle, buf.data_ptr() + 8 * n * first, first, cnt, items, stride,
+                                   st)
             fn()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -59,7 +66,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.reps
-            limbs = B * cnt
+            limbs = items * cnt
             out[f"{name}_{d}"] = {"us_per_call": round(ms * 1e3, 2), "limbs": limbs,
                                   "us_per_limb": round(ms * 1e3 / limbs, 4),
                                   "gbs": round(16.0 * n * limbs / (ms * 1e-3) / 1e9, 1)}
