@@ -98,6 +98,19 @@ int helr_decrypt(helr_ctx* ctx, const uint64_t* sk, const uint64_t* ct,
 int helr_encode_plain(helr_ctx* ctx, const int64_t* msg, uint64_t* pt,
                       int count, int level, void* stream);
 
+/* Device-side CKKS encoding (client side; replaces the
+ * host FFT behind SimContext.enc, hesim.py:146-158, as used by client_prepare,
+ * enctrain.py:114-152).  re / im (im may be NULL = real slots): count slot
+ * vectors of N/2 doubles at slot_stride; coef: count x N int64 = rint(scale *
+ * m) of the canonical-embedding polynomial (encoder.py).  Device pointers;
+ * synchronises the stream (it reports overflow: |scale * m| >= 2^62). */
+int helr_encode(helr_ctx* ctx, const double* re, const double* im, int64_t slot_stride, int count,
+                double scale, int64_t* coef, void* stream);
+/* Inverse map (SimContext.dec, hesim.py:160-162, via decode_weights,
+ * enctrain.py:266-289): integer coefficients -> slots / scale. */
+int helr_decode(helr_ctx* ctx, const int64_t* coef, int count, double scale, double* re, double* im,
+                int64_t slot_stride, void* stream);
+
 /* ---- arithmetic (SimContext.add/cadd/mul/cmul/imul, hesim.py:166-216) -- */
 
 int helr_add(helr_ctx* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out,

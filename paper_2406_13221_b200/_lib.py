@@ -42,6 +42,8 @@ SIGNATURES = {
     "helr_encrypt": [_vp, _u64p, _u64p, _u64p, _i, _i, _u64, _u64, _vp],
     "helr_decrypt": [_vp, _u64p, _u64p, _i, _i, _u64p, _vp],
     "helr_encode_plain": [_vp, _u64p, _u64p, _i, _i, _vp],
+    "helr_encode": [_vp, _vp, _vp, _i64, _i, ctypes.c_double, _vp, _vp],
+    "helr_decode": [_vp, _vp, _i, ctypes.c_double, _vp, _vp, _i64, _vp],
     "helr_add": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_sub": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_add_const": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],

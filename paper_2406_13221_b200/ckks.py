@@ -191,6 +191,44 @@ class GpuContext:
             self._residue_cache[key] = t
         return t
 
+    # ------------------------------------------------- device-side encoding
+    def encode_slots(self, values, scale: float) -> torch.Tensor:
+        """Device encoding (helr_encode): B slot vectors (real or complex,
+        at most N/2 values each, zero-padded) -> int64[B][N] coefficients on
+        the device, the device twin of ``encoder.encode`` (same embedding;
+        a coefficient may differ by one unit where the value is within
+        rounding error of a half-integer)."""
+        ck = self.ckks
+        if isinstance(values, torch.Tensor):
+            v = values.to(self.device)
+        else:
+            v = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(values))).to(self.device)
+        if v.dim() == 1:
+            v = v.unsqueeze(0)
+        if v.shape[-1] > ck.slots:
+            raise ValueError(f"message has {v.shape[-1]} slots, maximum is {ck.slots}")
+        cplx = v.is_complex()
+        re = torch.zeros((v.shape[0], ck.slots), dtype=torch.float64, device=self.device)
+        re[:, : v.shape[-1]] = v.real if cplx else v
+        im = None
+        if cplx:
+            im = torch.zeros_like(re)
+            im[:, : v.shape[-1]] = v.imag
+        coef = self._empty((v.shape[0], ck.n))
+        self._call("helr_encode", _ptr(re), _ptr(im) if im is not None else None, ck.slots, v.shape[0], float(scale),
+                   _ptr(coef), _stream())
+        return coef
+
+    def decode_coefficients(self, coef: torch.Tensor, scale: float) -> np.ndarray:
+        """Device decoding (helr_decode): int64[B][N] device coefficients ->
+        complex128[B][N/2] slots / scale."""
+        ck = self.ckks
+        c = coef.reshape(-1, ck.n).contiguous()
+        re = torch.empty((c.shape[0], ck.slots), dtype=torch.float64, device=self.device)
+        im = torch.empty_like(re)
+        self._call("helr_decode", _ptr(c), c.shape[0], float(scale), _ptr(re), _ptr(im), ck.slots, _stream())
+        return (re.cpu().numpy() + 1j * im.cpu().numpy())
+
     def _plain(self, coef: np.ndarray, level: int) -> torch.Tensor:
         ck = self.ckks
         msg = torch.from_numpy(np.ascontiguousarray(coef, dtype=np.int64)).to(self.device)
@@ -219,11 +257,13 @@ class GpuContext:
     def encrypt_to(self, coef: np.ndarray, dest: torch.Tensor, level: int) -> None:
         """Encrypt int64[B][N] coefficients into the contiguous device buffer
         ``dest`` (B x [2][L][N]); randomness ids are taken from the context."""
-        coef = np.ascontiguousarray(np.atleast_2d(coef), dtype=np.int64)
-        count = coef.shape[0]
+        if isinstance(coef, torch.Tensor):  # already on the device (encode_slots)
+            msg = coef.reshape(-1, self.ckks.n).to(device=self.device, dtype=torch.int64).contiguous()
+        else:
+            msg = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(coef), dtype=np.int64)).to(self.device)
+        count = msg.shape[0]
         if not dest.is_contiguous() or dest.numel() != count * 2 * self.ckks.L * self.ckks.n:
             raise ValueError("destination must be a contiguous batch of ciphertext buffers")
-        msg = torch.from_numpy(coef).to(self.device)
         first = self._take_ct_ids(count)
         self._call("helr_encrypt", _ptr(self.sk), _ptr(msg), _ptr(dest), count, level, self.enc_seed, first, _stream())
 

@@ -318,6 +318,9 @@ extern "C" int helr_ctx_destroy(helr_ctx* c) {
     cudaFree(c->d_modup_offs);
     cudaFree(c->ws);
     cudaFree(c->nag_ws);
+    cudaFree(c->enc_tw);
+    cudaFree(c->enc_tpos);
+    cudaFree(c->enc_tneg);
     delete c;
     return HELR_OK;
 }

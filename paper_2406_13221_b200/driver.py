@@ -181,7 +181,7 @@ class FusedTrainer:
                  mode: str = "mini_batch", poly: PolyApprox = BASELINE_CUBIC, schedule=None,
                  epsilon: float = 1e-8, enhanced: bool = True, use_graph: bool = False, bsgs: bool = True,
                  refresh_bits: int = 47, bsgs_bits: Optional[int] = None, rows_bits: Optional[int] = None,
-                 shard: tuple = (0, 1), reducer=None):
+                 shard: tuple = (0, 1), reducer=None, device_encode: bool = True):
         if mode not in ("mini_batch", "full_batch"):
             raise ValueError(f"mode must be mini_batch or full_batch, got {mode!r}")
         from .optimizer import ExpDecay
@@ -202,6 +202,9 @@ class FusedTrainer:
         if self.shard_world > 1 and reducer is None:
             raise ValueError("a sharded trainer needs a reducer (shard.ResidueAllReduce)")
         self.reducer = reducer
+        # client-side encoding on the device (helr_encode; encoder.py is the
+        # host twin, kept for comparisons)
+        self.device_encode = device_encode
         # W, V re-enter each iteration at scale 2^refresh_bits: above Delta = 2^40
         # so the refresh's fresh encryption noise is negligible, below 2^50 so
         # the row-start mask still encodes at >= 2^35
@@ -257,8 +260,9 @@ class FusedTrainer:
         nblk = lay.row_blocks * C
         flat = blocks.reshape(nblk, ck.slots)
         chunk = 64
+        encode = ctx.encode_slots if self.device_encode else ctx.encoder.encode
         for s in range(0, nblk, chunk):
-            coef = ctx.encoder.encode(flat[s:s + chunk], s_top)
+            coef = encode(flat[s:s + chunk], s_top)
             ctx.encrypt_to(coef, zflat[s:s + coef.shape[0]], top)
         if nb * R * C > nblk:  # zero blocks padding the last batch (encryptions of 0)
             pad = nb * R * C - nblk
@@ -281,7 +285,7 @@ class FusedTrainer:
         # stays ~2^-30 relative to B̄ (the planner tracks the exact scale)
         self.s_b = s_top / float(np.max(np.abs(bb)))
         for s in range(0, bflat.shape[0], chunk):
-            coef = ctx.encoder.encode(bflat[s:s + chunk], self.s_b)
+            coef = encode(bflat[s:s + chunk], self.s_b)
             ctx.encrypt_to(coef, bout[s:s + coef.shape[0]], top)
         # W0 = V0 = enc(0) at the top level (enctrain.py:145-151)
         self.wv = torch.empty((2 * C, 2, L, N), dtype=torch.int64, device=ctx.device)
@@ -565,10 +569,13 @@ class FusedTrainer:
             out = torch.empty((C, self.ck.n), dtype=torch.int64, device=ctx.device)
             ctx._call("helr_decrypt", ctx.sk.data_ptr(), self.wv.data_ptr(), C, self.level, out.data_ptr(),
                       self.stream.cuda_stream)
-            coef = out.cpu().numpy()
+            if self.device_encode:
+                slots = ctx.decode_coefficients(out, self.s_w)
+            else:
+                slots = ctx.encoder.decode(out.cpu().numpy(), self.s_w)
         segs = []
         for j in range(C):
-            grid = ctx.encoder.decode(coef[j], self.s_w).reshape(lay.m, lay.g)
+            grid = slots[j].reshape(lay.m, lay.g)
             segs.append(np.real(grid[0]))
         return np.concatenate(segs)[: lay.cols]
 
