@@ -117,7 +117,7 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
 #pragma unroll
                     for (int j = 0; j < ND; j++) {
                         double uh, ul;
-                        split21(*slot(stage, 2 * ND + b * ND + j), uh, ul);
+                        split21_d(__longlong_as_double((long long)*slot(stage, 2 * ND + b * ND + j)), uh, ul);
                         mac_d(a0[b], uh, ul, k0h[j], k0l[j]);
                         mac_d(a1[b], uh, ul, k1h[j], k1l[j]);
                     }
@@ -159,8 +159,8 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
             u64* ap = acc + (size_t)(b0 + b) * acc_item_stride;
             u64 o0, o1;
             if constexpr (DBL) {
-                o0 = reduce128(dresolve(a0[b]), q, r1, r0, osh);
-                o1 = reduce128(dresolve(a1[b]), q, r1, r0, osh);
+                o0 = reduce128(dresolve_s(a0[b]), q, r1, r0, osh);
+                o1 = reduce128(dresolve_s(a1[b]), q, r1, r0, osh);
             } else {
                 o0 = reduce128(resolve(a0[b]), q, r1, r0, osh);
                 o1 = reduce128(resolve(a1[b]), q, r1, r0, osh);

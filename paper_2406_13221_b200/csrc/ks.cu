@@ -79,13 +79,18 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
             const ulonglong2 c = ld2(coef + (size_t)p * a.n + i);
             y0[k] = shoup(c.x, hv[k], hvs[k], tb.q[p]);
             y1[k] = shoup(c.y, hv[k], hvs[k], tb.q[p]);
+            // own-digit limbs: the NTT-form input itself (exact doubles for fp64 limbs)
+            ulonglong2 v;
             if (a.galois) {
                 const u64* dp = d + (size_t)p * a.n;
-                st2(ext + (size_t)p * a.n + i, dp[galois_perm(i, (u64)a.galois, a.log_n)],
-                    dp[galois_perm(i + 1, (u64)a.galois, a.log_n)]);
+                v = make_ulonglong2(dp[galois_perm(i, (u64)a.galois, a.log_n)],
+                                    dp[galois_perm(i + 1, (u64)a.galois, a.log_n)]);
             } else {
-                *reinterpret_cast<ulonglong2*>(ext + (size_t)p * a.n + i) = ld2(d + (size_t)p * a.n + i);
+                v = ld2(d + (size_t)p * a.n + i);
             }
+            if (tb.q[p] < NTT_DBL_BOUND)
+                v = make_ulonglong2((u64)__double_as_longlong(u2d(v.x)), (u64)__double_as_longlong(u2d(v.y)));
+            *reinterpret_cast<ulonglong2*>(ext + (size_t)p * a.n + i) = v;
         }
     }
     // source residues as exact doubles (primes < 2^41) for the fp64 targets
@@ -120,7 +125,9 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
                     }
                 }
             }
-            st2(ext + (size_t)e * a.n + i, d2u_canon(s0, dc), d2u_canon(s1, dc));
+            // raw signed double (|x| <= q/2 + 1): the NTT below reads it as is (in_raw)
+            st2(ext + (size_t)e * a.n + i, (u64)__double_as_longlong(reduce_d(s0, dc)),
+                (u64)__double_as_longlong(reduce_d(s1, dc)));
             t++;
             continue;
         }
@@ -163,7 +170,8 @@ __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long 
             const ulonglong2 k1 = ld2(evk + (((size_t)j * 2 + 1) * LK + p) * n + i);
             const ulonglong2 u = ld2(xb + (size_t)j * ext_digit_stride);
             double uxh, uxl, uyh, uyl, k0xh, k0xl, k0yh, k0yl, k1xh, k1xl, k1yh, k1yl;
-            split21(u.x, uxh, uxl); split21(u.y, uyh, uyl);
+            split21_d(__longlong_as_double((long long)u.x), uxh, uxl);  // ext: exact doubles
+            split21_d(__longlong_as_double((long long)u.y), uyh, uyl);
             split21(k0.x, k0xh, k0xl); split21(k0.y, k0yh, k0yl);
             split21(k1.x, k1xh, k1xl); split21(k1.y, k1yh, k1yl);
             mac_d(c00, uxh, uxl, k0xh, k0xl);
@@ -171,10 +179,10 @@ __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long 
             mac_d(c10, uxh, uxl, k1xh, k1xl);
             mac_d(c11, uyh, uyl, k1yh, k1yl);
         }
-        o00 = reduce128(dresolve(c00), q, r1, r0, one_sh[p]);
-        o01 = reduce128(dresolve(c01), q, r1, r0, one_sh[p]);
-        o10 = reduce128(dresolve(c10), q, r1, r0, one_sh[p]);
-        o11 = reduce128(dresolve(c11), q, r1, r0, one_sh[p]);
+        o00 = reduce128(dresolve_s(c00), q, r1, r0, one_sh[p]);
+        o01 = reduce128(dresolve_s(c01), q, r1, r0, one_sh[p]);
+        o10 = reduce128(dresolve_s(c10), q, r1, r0, one_sh[p]);
+        o11 = reduce128(dresolve_s(c11), q, r1, r0, one_sh[p]);
     } else {
     u128v a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
     for (int j = 0; j < nd; j++) {
@@ -333,12 +341,14 @@ static int ks_modup(helr_ctx* c, KsInput in, int level, int B, const KsWs& w, cu
                 m.off[m.count] = (unsigned char)(j * c->LK + e);
                 m.prime[m.count] = (unsigned char)(e < nl ? e : L + (e - nl));
                 if (++m.count == HELR_MAXLIMBS) {
-                    ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s);
+                    ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s, 1, 1);
                     m.count = 0;
                 }
             }
         }
-        if (m.count) ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s);
+        // fp64 limbs: raw doubles in, exact (canonical) doubles out — the inner
+        // products split them on the fp64 pipe (split21_d)
+        if (m.count) ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s, 1, 1);
         CHECK_LAUNCH("ks modup ntt");
     }
     return HELR_OK;

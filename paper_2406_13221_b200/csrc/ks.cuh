@@ -98,6 +98,27 @@ __device__ __forceinline__ void mac_d(dacc& a, double xh, double xl, double yh, 
 __device__ __forceinline__ u64 dexact(double x) {  // integer-valued 0 <= x < 2^52
     return (u64)__double_as_longlong(__dadd_rn(x, NTT_TWO52)) & 0x000FFFFFFFFFFFFFull;
 }
+// ModUp'd digits of fp64 limbs are stored as exact doubles (ks_modup):
+// split x = h 2^21 + l with h = rint(x / 2^21) in [0, 2^20] and signed
+// l in [-2^20, 2^20] on the fp64 pipe (no integer shifts or masks).  The
+// partial products stay below 2^41 in magnitude; mid / ll may be negative.
+__device__ __forceinline__ void split21_d(double x, double& h, double& l) {
+    h = drint_mul(x, 4.76837158203125e-07);  // 2^-21
+    l = __fma_rn(-h, 2097152.0, x);
+}
+__device__ __forceinline__ long long dexact_s(double x) {  // integer-valued |x| < 2^51
+    return __double_as_longlong(__dadd_rn(x, NTT_MAGIC)) - 0x4338000000000000ll;
+}
+// hh 2^42 + mid 2^21 + ll with signed mid, ll (the total is non-negative)
+__device__ __forceinline__ u128acc dresolve_s(const dacc& a) {
+    const u64 H = dexact(a.hh);
+    const long long M = dexact_s(a.mid), Lo = dexact_s(a.ll);
+    u128acc r{H << 42, H >> 22};
+    const u64 m_lo = (u64)M << 21, m_hi = (u64)(M >> 43);
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r.lo), "+l"(r.hi) : "l"(m_lo), "l"(m_hi));
+    asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(r.lo), "+l"(r.hi) : "l"((u64)Lo), "l"((u64)(Lo >> 63)));
+    return r;
+}
 __device__ __forceinline__ u128acc dresolve(const dacc& a) {  // hh 2^42 + mid 2^21 + ll
     const u64 H = dexact(a.hh), M = dexact(a.mid), Lo = dexact(a.ll);
     u128acc r{H << 42, H >> 22};

@@ -38,6 +38,7 @@ struct NttPassArgs {
     // transform holds raw doubles (integer-valued, |x| < 2^46) instead of
     // canonical residues — saves the canonicalisation and the conversion back
     int raw_in, raw_out;
+    int dbl_out;  // fp64 limbs, final pass: canonical residues stored as exact doubles
 };
 
 template <int LOG_T, int LOG_R>
@@ -179,6 +180,11 @@ __device__ __forceinline__ u64 d2u_canon(double x, const DblC& c) {  // integer-
     double r = reduce_d(x, c);
     r = r < 0.0 ? __dadd_rn(r, c.q) : r;
     return (u64)__double_as_longlong(__dadd_rn(r, NTT_TWO52)) & 0x000FFFFFFFFFFFFFull;
+}
+// integer-valued |x| < 2^50 -> its residue in [0, q) as a double
+__device__ __forceinline__ double d2d_canon(double x, const DblC& c) {
+    const double r = reduce_d(x, c);
+    return r < 0.0 ? __dadd_rn(r, c.q) : r;
 }
 template <int R, int H>
 __device__ __forceinline__ void fwd_stage_d(double (&x)[R], const double* __restrict__ W, int tb0, const DblC& c) {
@@ -427,6 +433,8 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                 if constexpr (DBL) {
                     if (a.raw_out)  // forward: |x| < 10 q; inverse: reduce the 2^8 growth
                         y[i] = (u64)__double_as_longlong(INV ? reduce_d(x[i], dc) : x[i]);
+                    else if (a.dbl_out)
+                        y[i] = (u64)__double_as_longlong(d2d_canon(x[i], dc));
                     else
                         y[i] = d2u_canon(x[i], dc);  // canonical [0, q)
                 } else {
@@ -542,7 +550,7 @@ constexpr long long NTT_SMALL_GRID = 2 * 148;
 template <int LOG_T, bool IS_COL, bool INV, int S2, class Ld, class St>
 static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
                             int log_n, int st0, int final_out, int count, cudaStream_t s, int raw_in = 0,
-                            int raw_out = 0) {
+                            int raw_out = 0, int dbl_out = 0) {
     constexpr int LOG_R = LOG_T < 4 ? LOG_T : 4;
     constexpr int T = 1 << LOG_T;
     // column passes: 16 adjacent columns (128-byte rows); row passes: ~4096 elements per CTA
@@ -551,7 +559,7 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
     constexpr int COLS_S = COLS >= 4 ? COLS / 4 : 1;
     const int subs = IS_COL ? (1 << (log_n - LOG_T)) : (1 << (log_n - LOG_T));
     const int cols = subs < COLS ? subs : COLS;  // tiny rings: fewer sub-transforms than COLS
-    NttPassArgs a{log_n, st0, final_out, raw_in, raw_out};
+    NttPassArgs a{log_n, st0, final_out, raw_in, raw_out, dbl_out};
     count_launches(1);
     if (cols == COLS) {
         const long long full = (long long)(subs / COLS) * map.count * count;
@@ -571,9 +579,10 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
 
 template <bool INV, class Ld, class St>
 static void ntt_single(int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
-                       int count, cudaStream_t s) {
+                       int count, cudaStream_t s, int in_raw, int out_dbl) {
     switch (log_n) {
-#define HELR_SP(LT) case LT: ntt_pass_launch<LT, false, INV, 0>(ld, st, tb, map, log_n, 0, 1, count, s); break;
+#define HELR_SP(LT) \
+    case LT: ntt_pass_launch<LT, false, INV, 0>(ld, st, tb, map, log_n, 0, 1, count, s, in_raw, 0, out_dbl); break;
         HELR_SP(2) HELR_SP(3) HELR_SP(4) HELR_SP(5) HELR_SP(6) HELR_SP(7) HELR_SP(8) HELR_SP(9)
         HELR_SP(10) HELR_SP(11)
 #undef HELR_SP
@@ -583,14 +592,14 @@ static void ntt_single(int log_n, const Ld& ld, const St& st, const Tables& tb, 
 
 template <bool INV, class Ld, class St>
 static void ntt_col(int lt, int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
-                    int final_out, int count, cudaStream_t s, int raw_in, int raw_out) {
+                    int final_out, int count, cudaStream_t s, int raw_in, int raw_out, int dbl_out) {
     // column pass of log N = LN: LT = floor(LN / 2) stages (= lt), element stride 2^(LN - LT)
     (void)lt;
     switch (log_n) {
 #define HELR_CP(LN) \
     case LN: \
         ntt_pass_launch<(LN) / 2, true, INV, (LN) - (LN) / 2>(ld, st, tb, map, log_n, 0, final_out, count, s, raw_in, \
-                                                              raw_out); \
+                                                              raw_out, dbl_out); \
         break;
         HELR_CP(12) HELR_CP(13) HELR_CP(14) HELR_CP(15) HELR_CP(16)
 #undef HELR_CP
@@ -600,11 +609,13 @@ static void ntt_col(int lt, int log_n, const Ld& ld, const St& st, const Tables&
 
 template <bool INV, class Ld, class St>
 static void ntt_row(int lt, int log_n, const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
-                    int final_out, int count, cudaStream_t s, int raw_in, int raw_out) {
+                    int final_out, int count, cudaStream_t s, int raw_in, int raw_out, int dbl_out) {
     const int st0 = log_n - lt;
     switch (lt) {
 #define HELR_RP(LT) \
-    case LT: ntt_pass_launch<LT, false, INV, 0>(ld, st, tb, map, log_n, st0, final_out, count, s, raw_in, raw_out); break;
+    case LT: \
+        ntt_pass_launch<LT, false, INV, 0>(ld, st, tb, map, log_n, st0, final_out, count, s, raw_in, raw_out, dbl_out); \
+        break;
         HELR_RP(6) HELR_RP(7) HELR_RP(8) HELR_RP(9)
 #undef HELR_RP
         default: break;
@@ -614,31 +625,33 @@ static void ntt_row(int lt, int log_n, const Ld& ld, const St& st, const Tables&
 inline int ntt_split_s1(int log_n) { return log_n / 2; }
 
 template <bool INV, class Ld, class St>
+// in_raw: fp64 limbs arrive as raw integer-valued doubles (|x| < 2^50);
+// out_dbl: fp64 limbs leave as canonical residues stored as exact doubles
 static void ntt_launch(const helr_ctx* c, const Ld& ld, const St& st, u64* mid, long long mid_stride,
-                       const LimbMap& map, int count, cudaStream_t s) {
+                       const LimbMap& map, int count, cudaStream_t s, int in_raw = 0, int out_dbl = 0) {
     const int log_n = c->log_n;
     ProfScope ps(PROF_NTT, 16.0 * c->n * map.count * count, s);
     if (log_n <= 11) {
-        ntt_single<INV>(log_n, ld, st, c->t, map, count, s);
+        ntt_single<INV>(log_n, ld, st, c->t, map, count, s, in_raw, out_dbl);
         return;
     }
     const int s1 = ntt_split_s1(log_n), s2 = log_n - s1;
     StBuf smid{mid, mid_stride, map, c->n};
     LdBuf lmid{mid, mid_stride, map, c->n};
     if (!INV) {
-        ntt_col<false>(s1, log_n, ld, smid, c->t, map, 0, count, s, 0, 1);
-        ntt_row<false>(s2, log_n, lmid, st, c->t, map, 1, count, s, 1, 0);
+        ntt_col<false>(s1, log_n, ld, smid, c->t, map, 0, count, s, in_raw, 1, 0);
+        ntt_row<false>(s2, log_n, lmid, st, c->t, map, 1, count, s, 1, 0, out_dbl);
     } else {
-        ntt_row<true>(s2, log_n, ld, smid, c->t, map, 0, count, s, 0, 1);
-        ntt_col<true>(s1, log_n, lmid, st, c->t, map, 1, count, s, 1, 0);
+        ntt_row<true>(s2, log_n, ld, smid, c->t, map, 0, count, s, in_raw, 1, 0);
+        ntt_col<true>(s1, log_n, lmid, st, c->t, map, 1, count, s, 1, 0, out_dbl);
     }
 }
 
 // Plain buffer-to-buffer NTT (in-place when in == out).
 template <bool INV>
 static void ntt_buffers(const helr_ctx* c, const u64* in, long long in_stride, u64* out, long long out_stride,
-                        const LimbMap& map, int count, cudaStream_t s) {
+                        const LimbMap& map, int count, cudaStream_t s, int in_raw = 0, int out_dbl = 0) {
     LdBuf ld{in, in_stride, map, c->n};
     StBuf st{out, out_stride, map, c->n};
-    ntt_launch<INV>(c, ld, st, out, out_stride, map, count, s);
+    ntt_launch<INV>(c, ld, st, out, out_stride, map, count, s, in_raw, out_dbl);
 }
