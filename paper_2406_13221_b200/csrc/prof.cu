@@ -35,9 +35,17 @@ static unsigned long long g_launches = 0;
 void count_launches(int k) { g_launches += (unsigned long long)k; }
 extern "C" unsigned long long helr_launch_count(void) { return g_launches; }
 
+// external event nodes inside a graph capture, plain records otherwise
+static cudaError_t record(cudaEvent_t ev, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) cudaGetLastError();
+    return st == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
+                                               : cudaEventRecord(ev, s);
+}
+
 void prof_begin(int cat, double bytes, cudaStream_t s) {
     Rec r{cat, bytes, take(), take()};
-    cudaError_t e = cudaEventRecordWithFlags(r.a, s, cudaEventRecordExternal);
+    cudaError_t e = record(r.a, s);
     if (e != cudaSuccess) {
         fprintf(stderr, "[helr prof] cudaEventRecord(begin) failed: %s\n", cudaGetErrorString(e));
         cudaGetLastError();
@@ -49,7 +57,7 @@ void prof_begin(int cat, double bytes, cudaStream_t s) {
 
 void prof_end(cudaStream_t s) {
     if (g_open < 0) return;
-    cudaError_t e = cudaEventRecordWithFlags(g_recs[g_open].b, s, cudaEventRecordExternal);
+    cudaError_t e = record(g_recs[g_open].b, s);
     if (e != cudaSuccess) {
         fprintf(stderr, "[helr prof] cudaEventRecord(end) failed: %s\n", cudaGetErrorString(e));
         cudaGetLastError();

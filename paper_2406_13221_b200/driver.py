@@ -243,6 +243,7 @@ class FusedTrainer:
         self.z_host = None
         self.b_host = None
         self.copy_stream = None
+        self._d2h_ev = None
         self._prepare()
 
     # ------------------------------------------------------------ client side
@@ -342,6 +343,8 @@ class FusedTrainer:
             self.copy_stream = torch.cuda.Stream(device=self.ctx.device)
             self._zst = [self.zstage, torch.empty_like(self.zstage)]
             self._bst = [self.bstage, torch.empty_like(self.bstage)]
+            self.w_snap = torch.empty_like(self.wv)
+        self._d2h_ev = None
         self._buf = 0
         self._loaded = [None, None]   # (batch, bbar index) each buffer holds / is receiving
         self._ready = [None, None]    # copy finished (copy stream)
@@ -547,9 +550,38 @@ class FusedTrainer:
         if self.host_stream:
             # the step's result leaves the device: the updated weight ciphertexts
             lv = self.level + 1
-            self.w_host[:, :, :lv].copy_(self.wv[:, :, :lv], non_blocking=True)
+            self._read_back(lv)
         return dict(iteration=self.t, lr=lr, eta=eta, gamma=gamma, level_start=level_start,
                     level_after=self.level, refreshed=refreshed)
+
+    def _read_back(self, lv: int):
+        """The step's result leaves the device off the critical path: a
+        device-side snapshot of the active W, V limbs (one contiguous copy per
+        polynomial, on the compute stream), then its device-to-host copy on
+        the copy stream, overlapping the next iteration.  The snapshot is
+        rewritten only after the previous read-back has finished."""
+        if self._d2h_ev is not None:
+            self.stream.wait_event(self._d2h_ev)
+        for ci in range(self.wv.shape[0]):
+            for pi in range(2):
+                self.w_snap[ci, pi, :lv].copy_(self.wv[ci, pi, :lv], non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record(self.stream)
+        cs = self.copy_stream
+        cs.wait_event(ready)
+        with torch.cuda.stream(cs):
+            for ci in range(self.wv.shape[0]):
+                for pi in range(2):
+                    self.w_host[ci, pi, :lv].copy_(self.w_snap[ci, pi, :lv], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self._d2h_ev = ev
+
+    def finish_host_stream(self):
+        """Order the compute stream after the last weight read-back (call
+        before recording the end of a timed e2e region)."""
+        if self._d2h_ev is not None:
+            self.stream.wait_event(self._d2h_ev)
 
     def combine_gradient(self):
         """Sum the ranks' partial gradients (raw residue words, exact in 63
