@@ -240,10 +240,22 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
             const u64 pk = tb.q[L + k];
             const double inv = __longlong_as_double((long long)pinv_dbl[k]);
             const ulonglong2 x = ld2(ap + (size_t)(nl + k) * n + i);
-            z0[k] = shoup(x.x, phinv[k], phinv_sh[k], pk);
-            z1[k] = shoup(x.y, phinv[k], phinv_sh[k], pk);
-            v0 = __dadd_rn(v0, __dmul_rn(__ull2double_rn(z0[k]), inv));
-            v1 = __dadd_rn(v1, __dmul_rn(__ull2double_rn(z1[k]), inv));
+            double d0, d1;  // canonical z as exact doubles (no u64 -> f64 conversions)
+            if (pk < NTT_DBL_BOUND) {
+                const DblC dk{tb.qd[L + k], tb.qinvd[L + k]};
+                const double w = u2d(phinv[k]);
+                d0 = d2d_canon(mulmod_d(u2d(x.x), w, dk), dk);
+                d1 = d2d_canon(mulmod_d(u2d(x.y), w, dk), dk);
+                z0[k] = dexact(d0);
+                z1[k] = dexact(d1);
+            } else {
+                z0[k] = shoup(x.x, phinv[k], phinv_sh[k], pk);
+                z1[k] = shoup(x.y, phinv[k], phinv_sh[k], pk);
+                d0 = __ull2double_rn(z0[k]);
+                d1 = __ull2double_rn(z1[k]);
+            }
+            v0 = __dadd_rn(v0, __dmul_rn(d0, inv));
+            v1 = __dadd_rn(v1, __dmul_rn(d1, inv));
         }
     }
     const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
@@ -273,7 +285,9 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
                     s1 = __dadd_rn(s1, mulmod_d(zd1[k], wd, dc));
                 }
             }
-            st2(mp + (size_t)p * n + i, d2u_canon(s0, dc), d2u_canon(s1, dc));
+            // raw signed doubles: the NTT that follows reads them as is (in_raw)
+            st2(mp + (size_t)p * n + i, (u64)__double_as_longlong(reduce_d(s0, dc)),
+                (u64)__double_as_longlong(reduce_d(s1, dc)));
             continue;
         }
         u64 s0 = 0, s1 = 0;
@@ -391,7 +405,7 @@ static int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const
         st.add_p = ep.add_p; st.p_is = ep.add_p_stride;
         st.ngal = ep.add_p ? ep.ngal : 0;
         for (int t = 0; t < HELR_MAX_HOIST; t++) st.gal[t] = ep.gal[t];
-        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s);
+        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s, 1);
         CHECK_LAUNCH("ks moddown ntt+final");
     }
     return HELR_OK;
@@ -458,10 +472,23 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
             const u64 m = tb.q[k < K ? L + k : l];
             const double inv = __longlong_as_double((long long)mt.dinv[k]);
             const ulonglong2 x = ld2(ap + (size_t)lim * n + i);
-            z0[k] = shoup(x.x, mt.hv[k], mt.hvs[k], m);
-            z1[k] = shoup(x.y, mt.hv[k], mt.hvs[k], m);
-            v0 = __dadd_rn(v0, __dmul_rn(__ull2double_rn(z0[k]), inv));
-            v1 = __dadd_rn(v1, __dmul_rn(__ull2double_rn(z1[k]), inv));
+            double d0, d1;  // canonical z as exact doubles (no u64 -> f64 conversions)
+            if (m < NTT_DBL_BOUND) {
+                const int pm = k < K ? L + k : l;
+                const DblC dk{tb.qd[pm], tb.qinvd[pm]};
+                const double w = u2d(mt.hv[k]);
+                d0 = d2d_canon(mulmod_d(u2d(x.x), w, dk), dk);
+                d1 = d2d_canon(mulmod_d(u2d(x.y), w, dk), dk);
+                z0[k] = dexact(d0);
+                z1[k] = dexact(d1);
+            } else {
+                z0[k] = shoup(x.x, mt.hv[k], mt.hvs[k], m);
+                z1[k] = shoup(x.y, mt.hv[k], mt.hvs[k], m);
+                d0 = __ull2double_rn(z0[k]);
+                d1 = __ull2double_rn(z1[k]);
+            }
+            v0 = __dadd_rn(v0, __dmul_rn(d0, inv));
+            v1 = __dadd_rn(v1, __dmul_rn(d1, inv));
         }
     }
     const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
@@ -490,7 +517,8 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
                     s1 = __dadd_rn(s1, mulmod_d(zd1[k], wd, dc));
                 }
             }
-            st2(mp + (size_t)p * n + i, d2u_canon(s0, dc), d2u_canon(s1, dc));
+            st2(mp + (size_t)p * n + i, (u64)__double_as_longlong(reduce_d(s0, dc)),
+                (u64)__double_as_longlong(reduce_d(s1, dc)));  // raw (in_raw NTT)
             continue;
         }
         u64 s0 = 0, s1 = 0;
@@ -539,7 +567,7 @@ static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, in
     {
         LdBuf ld{w.mdc, w.mdc_s, mq, n};
         const StCombine st = st_combine(c, out, os, (long long)L * n, w.acc, w.acc_s, (long long)ne * n, mt.mi, mt.mis, l);
-        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s);
+        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s, 1);
         CHECK_LAUNCH("mdr ntt+final");
     }
     return HELR_OK;
