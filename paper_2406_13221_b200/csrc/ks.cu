@@ -361,8 +361,20 @@ static int ks_modup(helr_ctx* c, KsInput in, int level, int B, const KsWs& w, cu
             }
         }
         // fp64 limbs: raw doubles in, exact (canonical) doubles out — the inner
-        // products split them on the fp64 pipe (split21_d)
-        if (m.count) ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s, 1, 1);
+        // products split them on the fp64 pipe (split21_d).  Integer-path
+        // limbs (q_0) first: the limb is the grid's slowest index, so the
+        // slower CTAs start in the first waves.
+        if (m.count) {
+            LimbMap h;
+            h.count = 0;
+            for (int pass = 0; pass < 2; pass++)
+                for (int i = 0; i < m.count; i++)
+                    if ((c->primes[m.prime[i]] >= NTT_DBL_BOUND) == (pass == 0)) {
+                        h.off[h.count] = m.off[i];
+                        h.prime[h.count++] = m.prime[i];
+                    }
+            ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, h, B, s, 1, 1);
+        }
         CHECK_LAUNCH("ks modup ntt");
     }
     return HELR_OK;

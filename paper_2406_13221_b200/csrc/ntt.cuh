@@ -481,6 +481,13 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
     }
 }
 
+#ifndef NTT_LIMB_MAJOR
+#define NTT_LIMB_MAJOR 1
+#endif
+static inline dim3 ntt_grid(int tiles, int limbs, int items) {
+    return NTT_LIMB_MAJOR ? dim3(tiles, items, limbs) : dim3(tiles, limbs, items);
+}
+
 template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, class Ld, class St>
 #ifndef HELR_NTT_MINB
 #define HELR_NTT_MINB 4  // resident 256-thread CTAs per SM the register budget is sized for
@@ -490,10 +497,14 @@ __global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R),
 ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     constexpr int T = 1 << LOG_T;
     __shared__ u64 sm[IS_COL ? T * (COLS + 1) : COLS * (T + T / 16)];
-    if (tb.q[map.prime[blockIdx.y]] < NTT_DBL_BOUND)
-        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true>(ld, st, tb, map, a, sm, blockIdx.x, blockIdx.y, blockIdx.z);
+    // grid: x = tiles, y = batch item, z = limb (NTT_LIMB_MAJOR) — the limb is
+    // the slowest index, so the slower integer-path limb (q_0, listed first)
+    // is scheduled in the first waves rather than in the tail
+    const int li = NTT_LIMB_MAJOR ? blockIdx.z : blockIdx.y, z = NTT_LIMB_MAJOR ? blockIdx.y : blockIdx.z;
+    if (tb.q[map.prime[li]] < NTT_DBL_BOUND)
+        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true>(ld, st, tb, map, a, sm, blockIdx.x, li, z);
     else
-        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, false>(ld, st, tb, map, a, sm, blockIdx.x, blockIdx.y, blockIdx.z);
+        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, false>(ld, st, tb, map, a, sm, blockIdx.x, li, z);
 }
 
 // ---- plain functors: strided limb buffers -------------------------------
@@ -564,15 +575,15 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
     if (cols == COLS) {
         const long long full = (long long)(subs / COLS) * map.count * count;
         if (COLS_S < COLS && full < NTT_SMALL_GRID && log_n >= 12) {
-            dim3 grid(subs / COLS_S, map.count, count);
+            dim3 grid = ntt_grid(subs / COLS_S, map.count, count);
             ntt_pass<LOG_T, LOG_R, COLS_S, IS_COL, INV, S2><<<grid, T * COLS_S / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
             return;
         }
-        dim3 grid(subs / COLS, map.count, count);
+        dim3 grid = ntt_grid(subs / COLS, map.count, count);
         ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV, S2><<<grid, T * COLS / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
     } else {
         // only reachable for single-pass rings (subs == 1)
-        dim3 grid(subs / cols, map.count, count);
+        dim3 grid = ntt_grid(subs / cols, map.count, count);
         ntt_pass<LOG_T, LOG_R, 1, IS_COL, INV, S2><<<grid, T / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
     }
 }
