@@ -80,6 +80,39 @@ struct helr_ctx {
     int* enc_tneg = nullptr;  // [N/2]
 };
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Every kernel of the iteration starts with pdl_begin(): wait until the
+// previous kernel in the stream has completed and its writes are visible.
+// Launched through launch_pdl (cudaLaunchAttributeProgrammaticStreamSerialization)
+// the next kernel's launch is processed while its predecessor runs (the
+// trigger fires implicitly at the predecessor's completion; an explicit early
+// trigger, which lets waiting CTAs occupy SMs during the last wave, measured
+// 1 % slower); inside a captured graph the edges become programmatic.
+// Measured: 190.7 -> 192.9 it/s.  HELR_PDL=0 turns the attribute off.
+#ifndef HELR_PDL_TRIGGER
+#define HELR_PDL_TRIGGER 0  // early trigger measured slower (dependents idle on SMs)
+#endif
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (HELR_PDL_TRIGGER) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 void set_error(const std::string& msg);
 bool cuda_ok(cudaError_t e, const char* what);
 void clear_stale_error(const char* where);

@@ -179,6 +179,7 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
 
 template <int ND, int NB>
 __global__ void __launch_bounds__(HOIST_T, 3) k_ks_inner_hoisted(HoistKeys hk, HoistArgs A, Tables tb) {
+    pdl_begin();
     const int e = blockIdx.y;
     const int p = e < A.nl ? e : A.L + (e - A.nl);
     if (tb.q[p] < NTT_DBL_BOUND)  // uniform per CTA (one limb per CTA)
@@ -211,7 +212,7 @@ static void launch_hoisted_nb(dim3 g, cudaStream_t s, const HoistKeys& hk, Hoist
         attr = true;
     }
     g.x *= A.nchunks;
-    k_ks_inner_hoisted<ND, NB><<<g, HOIST_T, smem, s>>>(hk, A, tb);
+    launch_pdl(k_ks_inner_hoisted<ND, NB>, g, dim3(HOIST_T), smem, s, hk, A, tb);
 }
 // ciphertexts per thread: HELR_HOIST_NB (1, 2, 4 or 8; default 4) caps it
 static int hoist_nb_cap() {

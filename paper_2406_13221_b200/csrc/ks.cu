@@ -56,6 +56,7 @@ struct ModUpArgs {
 
 template <int MA>
 __global__ void k_modup(ModUpArgs a, Tables tb) {
+    pdl_begin();
     const int j = blockIdx.y, b = blockIdx.z;
     const int lo = j * a.alpha, hi = lo + a.alpha < a.nl ? lo + a.alpha : a.nl;
     const int ns = hi - lo;
@@ -155,6 +156,7 @@ __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long 
                            u64* acc, long long acc_item_stride, int n, int nl, int K, int L, int LK, int nd, int B,
                            Tables tb, const u64* dadd, long long dadd_is, const u64* pm, const u64* pm_sh,
                            const u64* one_sh) {
+    pdl_begin();
     const int e = blockIdx.y;
     const int b = blockIdx.z * blockDim.y + threadIdx.y;
     const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
@@ -225,6 +227,7 @@ template <int MK>
 __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n,
                                int nl, int K, int L, const u64* phinv, const u64* phinv_sh, const u64* phm,
                                const u64* phms, const u64* pinv_dbl, const u64* pm, const u64* pm_sh, Tables tb) {
+    pdl_begin();
     const int it = blockIdx.y;  // item*2 + poly
     const int b = it >> 1, poly = it & 1;
     const int ne = nl + K;
@@ -339,9 +342,9 @@ static int ks_modup(helr_ctx* c, KsInput in, int level, int B, const KsWs& w, cu
                     c->d_modup_offs + (size_t)level * c->beta, n, c->log_n, nl, K, L, c->alpha};
         dim3 g(blocks_for(n / 2, 128), nd, B);
         ProfScope ps(PROF_MODUP, 8.0 * n * B * (2.0 * nl + (double)nd * ne), s);
-        if (c->alpha <= 4) k_modup<4><<<g, 128, 0, s>>>(a, c->t);
-        else if (c->alpha <= 8) k_modup<8><<<g, 128, 0, s>>>(a, c->t);
-        else k_modup<HELR_MAXP><<<g, 128, 0, s>>>(a, c->t);
+        if (c->alpha <= 4) launch_pdl(k_modup<4>, g, dim3(128), 0, s, a, c->t);
+        else if (c->alpha <= 8) launch_pdl(k_modup<8>, g, dim3(128), 0, s, a, c->t);
+        else launch_pdl(k_modup<HELR_MAXP>, g, dim3(128), 0, s, a, c->t);
         CHECK_KERNEL("ks modup");
     }
     // 3) NTT of every converted limb of every digit (one launch per 128 limbs)
@@ -396,8 +399,8 @@ static int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const
     {
         ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + nl), s);
         auto conv = K <= 4 ? k_moddown_conv<4> : (K <= 8 ? k_moddown_conv<8> : k_moddown_conv<HELR_MAXP>);
-        conv<<<g, 128, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv, c->md_phinv_sh, c->md_phmod,
-                               c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
+        launch_pdl(conv, g, dim3(128), 0, s, (const u64*)w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv,
+                   c->md_phinv_sh, c->md_phmod, c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
         CHECK_KERNEL("ks moddown conv");
     }
     LimbMap mq;
@@ -434,8 +437,8 @@ static int key_inner_single(helr_ctx* c, const KsWs& w, const u64* evk, int B, i
     dim3 g(blocks_for(n / 2, 64), ne, (B + by - 1) / by);
     ProfScope ps(PROF_INNER, 8.0 * n * ((double)B * nd * ne + 2.0 * nd * ne + 2.0 * B * ne + (dadd ? 2.0 * B * nl : 0.0)),
                  s);
-    k_ks_inner<<<g, dim3(64, by), 0, s>>>(w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L, c->LK, nd, B,
-                                          c->t, dadd, dadd_is, c->pmod, c->pmod_sh, c->one_sh);
+    launch_pdl(k_ks_inner, g, dim3(64, by), 0, s, (const u64*)w.ext, w.ext_s, w.ext_ds, evk, w.acc, w.acc_s, n, nl, K, L,
+               c->LK, nd, B, c->t, dadd, dadd_is, c->pmod, c->pmod_sh, c->one_sh);
     CHECK_KERNEL("ks inner");
     return HELR_OK;
 }
@@ -468,6 +471,7 @@ static MrTab mr_tab(const helr_ctx* c, int level) {
 template <int MK>
 __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n, int nl,
                            int K, int L, MrTab mt, Tables tb) {
+    pdl_begin();
     const int it = blockIdx.y;  // item*2 + poly
     const int b = it >> 1, poly = it & 1;
     const int ne = nl + K, l = nl - 1, ns = K + 1;
@@ -566,7 +570,7 @@ static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, in
         dim3 g(blocks_for(n / 2, 128), 2 * B);
         ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + 1 + l), s);
         auto conv = K + 1 <= 4 ? k_mdr_conv<4> : (K + 1 <= 8 ? k_mdr_conv<8> : k_mdr_conv<HELR_MAXP>);
-        conv<<<g, 128, 0, s>>>(w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, mt, c->t);
+        launch_pdl(conv, g, dim3(128), 0, s, (const u64*)w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, mt, c->t);
         CHECK_KERNEL("mdr conv");
     }
     LimbMap mq;
@@ -648,6 +652,7 @@ struct TensorArgs {
     int terms;
 };
 __global__ void k_tensor(TensorArgs ta, u64* d, int n, int L, Tables tb) {
+    pdl_begin();
     const int p = blockIdx.y, it = blockIdx.z;
     const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
     u64* d0 = d + (size_t)it * 3 * L * n + (size_t)p * n;
@@ -707,7 +712,7 @@ int op_mul_relin_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, 
         TensorArgs ta{a + (size_t)b0 * a_is, a_is, a_ts, b + (size_t)b0 * b_is, b_is, b_ts, terms};
         {
             ProfScope ps(PROF_TENSOR, 8.0 * c->n * nb * (level + 1) * (4.0 * terms + 3.0), s);
-            k_tensor<<<g, 256, 0, s>>>(ta, w.tensor, c->n, c->L, c->t);
+            launch_pdl(k_tensor, g, dim3(256), 0, s, ta, w.tensor, c->n, c->L, c->t);
             CHECK_KERNEL("tensor");
         }
         const long long ts = 3ll * c->L * c->n;
@@ -744,7 +749,7 @@ int op_mul_relin_rescale_sum(helr_ctx* c, const u64* a, long long a_is, long lon
             dim3 g(blocks_for(n, 256), level + 1, nb);
             ProfScope ps(PROF_TENSOR, 8.0 * n * nb * (level + 1) * (4.0 * terms + 3.0), s);
             TensorArgs ta{a + (size_t)b0 * a_is, a_is, a_ts, b + (size_t)b0 * b_is, b_is, b_ts, terms};
-            k_tensor<<<g, 256, 0, s>>>(ta, w.tensor, n, L, c->t);
+            launch_pdl(k_tensor, g, dim3(256), 0, s, ta, w.tensor, n, L, c->t);
             CHECK_KERNEL("tensor");
         }
         const long long ts = 3ll * L * n;

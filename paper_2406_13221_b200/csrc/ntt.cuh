@@ -495,6 +495,7 @@ template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, class L
 __global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R),
                                   ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 256 ? HELR_NTT_MINB : 1)
 ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
+    pdl_begin();
     constexpr int T = 1 << LOG_T;
     __shared__ u64 sm[IS_COL ? T * (COLS + 1) : COLS * (T + T / 16)];
     // grid: x = tiles, y = batch item, z = limb (NTT_LIMB_MAJOR) — the limb is
@@ -576,15 +577,17 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
         const long long full = (long long)(subs / COLS) * map.count * count;
         if (COLS_S < COLS && full < NTT_SMALL_GRID && log_n >= 12) {
             dim3 grid = ntt_grid(subs / COLS_S, map.count, count);
-            ntt_pass<LOG_T, LOG_R, COLS_S, IS_COL, INV, S2><<<grid, T * COLS_S / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
+            launch_pdl(ntt_pass<LOG_T, LOG_R, COLS_S, IS_COL, INV, S2, Ld, St>, grid, dim3(T * COLS_S / (1 << LOG_R)), 0, s, ld, st,
+                       tb, map, a);
             return;
         }
         dim3 grid = ntt_grid(subs / COLS, map.count, count);
-        ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV, S2><<<grid, T * COLS / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
+        launch_pdl(ntt_pass<LOG_T, LOG_R, COLS, IS_COL, INV, S2, Ld, St>, grid, dim3(T * COLS / (1 << LOG_R)), 0, s, ld, st, tb,
+                   map, a);
     } else {
         // only reachable for single-pass rings (subs == 1)
         dim3 grid = ntt_grid(subs / cols, map.count, count);
-        ntt_pass<LOG_T, LOG_R, 1, IS_COL, INV, S2><<<grid, T / (1 << LOG_R), 0, s>>>(ld, st, tb, map, a);
+        launch_pdl(ntt_pass<LOG_T, LOG_R, 1, IS_COL, INV, S2, Ld, St>, grid, dim3(T / (1 << LOG_R)), 0, s, ld, st, tb, map, a);
     }
 }
 

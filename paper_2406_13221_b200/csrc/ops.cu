@@ -40,6 +40,7 @@ __device__ __forceinline__ void ew_decode(long long idx, const EwGeom& g, int& i
 
 __global__ void k_elementwise(int op, const u64* a, const u64* b, u64* out, EwGeom g, long long total,
                               Tables tb, const u64* imul_f) {
+    pdl_begin();
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         int item, poly, limb, k;
@@ -79,7 +80,7 @@ int op_ew(helr_ctx* c, int op, const u64* a, long long as, const u64* b, long lo
     if (blocks > 148 * 16) blocks = 148 * 16;
     ProfScope ps(PROF_ELEM, 8.0 * total * ((op == EW_ADD || op == EW_SUB) ? 3 : 2), s);
     if (op == EW_REDUCE) b = a;  // unary
-    k_elementwise<<<blocks, 256, 0, s>>>(op, a, b, out, g, total, c->t, c->imul_f);
+    launch_pdl(k_elementwise, dim3(blocks), dim3(256), 0, s, op, a, b, out, g, total, c->t, c->imul_f);
     CHECK_KERNEL("elementwise");
     return HELR_OK;
 }
@@ -261,6 +262,7 @@ extern "C" int helr_keygen_switch(helr_ctx* c, const uint64_t* sk, int64_t galoi
 // encryption / decryption
 __global__ void k_enc_fill(u64* ct, const long long* msg, int n, int L, int nl, u64 seed, u64 first_id, int eta,
                            Tables tb) {
+    pdl_begin();
     const int b = blockIdx.y;
     const u64 key = prng_key(seed, stream_id(ST_CT, first_id + (u64)b, 0, PU_E));
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -269,6 +271,7 @@ __global__ void k_enc_fill(u64* ct, const long long* msg, int n, int L, int nl, 
     }
 }
 __global__ void k_enc_combine(u64* ct, const u64* sk, int n, int L, u64 seed, u64 first_id, Tables tb) {
+    pdl_begin();
     const int b = blockIdx.z, p = blockIdx.y;
     const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
     const u64 key = prng_key(seed, stream_id(ST_CT, first_id + (u64)b, 0, PU_A));
@@ -286,14 +289,14 @@ __global__ void k_enc_combine(u64* ct, const u64* sk, int n, int L, u64 seed, u6
 static int encrypt_dev(helr_ctx* c, const u64* sk, const long long* msg, u64* ct, int count, int level, u64 seed,
                        u64 first_id, cudaStream_t s) {
     dim3 g1(blocks_for(c->n, 256), count);
-    k_enc_fill<<<g1, 256, 0, s>>>(ct, msg, c->n, c->L, level + 1, seed, first_id, c->eta, c->t);
+    launch_pdl(k_enc_fill, g1, dim3(256), 0, s, ct, msg, c->n, c->L, level + 1, seed, first_id, c->eta, c->t);
     CHECK_KERNEL("encrypt fill");
     LimbMap m = limb_range(0, level + 1);
     const long long st = 2ll * c->L * c->n;
     ntt_buffers<false>(c, ct, st, ct, st, m, count, s);
     CHECK_LAUNCH("encrypt ntt");
     dim3 g2(blocks_for(c->n, 256), level + 1, count);
-    k_enc_combine<<<g2, 256, 0, s>>>(ct, sk, c->n, c->L, seed, first_id, c->t);
+    launch_pdl(k_enc_combine, g2, dim3(256), 0, s, ct, sk, c->n, c->L, seed, first_id, c->t);
     CHECK_KERNEL("encrypt combine");
     return HELR_OK;
 }
@@ -307,6 +310,7 @@ extern "C" int helr_encrypt(helr_ctx* c, const uint64_t* sk, const int64_t* msg,
 }
 
 __global__ void k_dec_combine(const u64* ct, const u64* sk, u64* v, int n, int L, Tables tb) {
+    pdl_begin();
     const int b = blockIdx.y;
     const u64 q = tb.q[0], r1 = tb.br1[0], r0 = tb.br0[0];
     const u64* c0 = ct + (size_t)b * 2 * L * n;
@@ -315,6 +319,7 @@ __global__ void k_dec_combine(const u64* ct, const u64* sk, u64* v, int n, int L
         v[(size_t)b * n + i] = add_mod(c0[i], mul_mod(c1[i], sk[i], q, r1, r0), q);
 }
 __global__ void k_center(const u64* v, long long* out, long long total, double ratio, Tables tb) {
+    pdl_begin();
     const u64 q = tb.q[0];
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -328,13 +333,14 @@ __global__ void k_center(const u64* v, long long* out, long long total, double r
 static int decrypt_dev(helr_ctx* c, const u64* sk, const u64* ct, int count, long long* out, double ratio,
                        u64* tmp, cudaStream_t s) {
     dim3 g(blocks_for(c->n, 256), count);
-    k_dec_combine<<<g, 256, 0, s>>>(ct, sk, tmp, c->n, c->L, c->t);
+    launch_pdl(k_dec_combine, g, dim3(256), 0, s, ct, sk, tmp, c->n, c->L, c->t);
     CHECK_KERNEL("decrypt combine");
     LimbMap m = limb_range(0, 1);
     ntt_buffers<true>(c, tmp, c->n, tmp, c->n, m, count, s);
     CHECK_LAUNCH("decrypt intt");
     long long total = (long long)count * c->n;
-    k_center<<<blocks_for(total, 256) < 4096 ? blocks_for(total, 256) : 4096, 256, 0, s>>>(tmp, out, total, ratio, c->t);
+    launch_pdl(k_center, dim3(blocks_for(total, 256) < 4096 ? blocks_for(total, 256) : 4096), dim3(256), 0, s, (const u64*)tmp,
+               out, total, ratio, c->t);
     CHECK_KERNEL("decrypt center");
     return HELR_OK;
 }
@@ -396,6 +402,7 @@ extern "C" int helr_refresh(helr_ctx* c, const uint64_t* sk, const uint64_t* a, 
 // rescale: out_i = (x_i - NTT_i([INTT_l(x_l)]_centred mod q_i)) * q_l^-1
 // (the combine runs in the storer of the last NTT pass, StCombine)
 __global__ void k_rescale_conv(const u64* r, u64* t, int n, int l, Tables tb) {
+    pdl_begin();
     // r: [items][N] coefficient form mod q_l;  t: [items][l][N]
     const int it = blockIdx.y;
     const u64 ql = tb.q[l], half = ql >> 1;
@@ -436,7 +443,7 @@ static int rescale_dev(helr_ctx* c, const u64* a, long long as, u64* out, long l
     dim3 g1(blocks_for(n, 256), items);
     {
         ProfScope ps(PROF_RESCALE, 8.0 * n * items * (1 + l), s);
-        k_rescale_conv<<<g1, 256, 0, s>>>(r, t, n, l, c->t);
+        launch_pdl(k_rescale_conv, g1, dim3(256), 0, s, (const u64*)r, t, n, l, c->t);
         CHECK_KERNEL("rescale conv");
     }
     // NTT of the converted limbs; the last pass finishes the rescale in its storer
@@ -475,6 +482,7 @@ struct LinArgs {
     int terms;
 };
 __global__ void k_lincomb(LinArgs la, u64* out, long long os, int n, int L, Tables tb) {
+    pdl_begin();
     const int p = blockIdx.y, it = blockIdx.z;  // it = item*2 + poly
     const int item = it >> 1, poly = it & 1;
     const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
@@ -499,7 +507,7 @@ int op_lincomb(helr_ctx* c, int terms, const u64* const* x, const long long* xs,
     la.terms = terms;
     dim3 g(blocks_for(c->n, 256), level + 1, 2 * count);
     ProfScope ps(PROF_ELEM, 8.0 * c->n * 2.0 * count * (level + 1) * (terms + 1), s);
-    k_lincomb<<<g, 256, 0, s>>>(la, out, os, c->n, c->L, c->t);
+    launch_pdl(k_lincomb, g, dim3(256), 0, s, la, out, os, c->n, c->L, c->t);
     CHECK_KERNEL("lincomb");
     return HELR_OK;
 }

@@ -1,5 +1,6 @@
 // prof.cu — event-pair recorder behind prof.cuh and its C ABI.
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/helr_ckks.h"
@@ -34,6 +35,15 @@ bool prof_enabled() { return g_on; }
 static unsigned long long g_launches = 0;
 void count_launches(int k) { g_launches += (unsigned long long)k; }
 extern "C" unsigned long long helr_launch_count(void) { return g_launches; }
+
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("HELR_PDL");
+        on = e ? (atoi(e) != 0) : 1;
+    }
+    return on != 0;
+}
 
 // external event nodes inside a graph capture, plain records otherwise
 static cudaError_t record(cudaEvent_t ev, cudaStream_t s) {
