@@ -241,6 +241,17 @@ int helr_nag_graph_capture(helr_ctx* ctx, const helr_nag_args* args, void* strea
 int helr_nag_graph_launch(void* graph_exec, void* stream);
 int helr_nag_graph_destroy(void* graph_exec);
 
+/* ---- training-harness metrics on the device ----
+ * The per-iteration metrics of train_encrypted (enctrain.py:417-436):
+ * scores s = X w (X: n x d row-major doubles, bias column included; y in
+ * {-1,+1}; w: d doubles; device pointers).  out (host, 4 doubles):
+ * log_likelihood (optim.py:123-126), accuracy of sign(s) (optim.py:200-206),
+ * midrank AUROC (optim.py:209-229; NaN with one class), n_pos.  scratch:
+ * helr_metrics_scratch(n) device doubles.  Synchronises the stream. */
+size_t helr_metrics_scratch(int n);
+int helr_metrics(helr_ctx* ctx, const double* X, const double* y, const double* w, int n, int d,
+                 double* scratch, double* out, void* stream);
+
 /* ---- instrumentation (not part of the reference surface) ---------------- */
 
 /* Per-launch CUDA-event timing by kernel category (0 NTT, 1 ModUp, 2 key

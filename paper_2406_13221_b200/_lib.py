@@ -51,6 +51,8 @@ SIGNATURES = {
     "helr_mul_const": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_plain": [_vp, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_reduce": [_vp, _u64p, _u64p, _i, _i, _vp],
+    "helr_metrics": [_vp, _vp, _vp, _vp, _i, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp],
+    "helr_metrics_scratch": None,  # returns size_t (bound in metrics.py)
     "helr_rescale": [_vp, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_relin": [_vp, _u64p, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_relin_rescale": [_vp, _u64p, _u64p, _u64p, _u64p, _i, _i, _vp],
