@@ -36,6 +36,10 @@ RINGS = {
     "n2e12": CkksParams.generate(log_n=12, n_q=5, dnum=2),
     "n2e15": CkksParams.generate(log_n=15, n_q=6, dnum=3),
     "n2e16": CkksParams.generate(log_n=16, n_q=8, dnum=3),
+    # BASELINE primitive-sweep rings: 50-60-bit primes, so every limb takes the
+    # integer (Shoup / 128-bit accumulator) path; dnum 1 and 3, L 16 and 24
+    "sweep_i50": CkksParams.generate(log_n=14, n_q=16, dnum=1, scale_bits=50, p_bits=60),
+    "sweep_l24": CkksParams.generate(log_n=14, n_q=24, dnum=3, scale_bits=55, p_bits=60),
 }
 
 
