@@ -557,7 +557,13 @@ struct StBuf {
 // Launches of fewer than NTT_SMALL_GRID full-size CTAs (single-ciphertext
 // key switches at low levels) use CTAs a quarter the size, so four times as
 // many SMs share the latency-bound work.
-constexpr long long NTT_SMALL_GRID = 2 * 148;
+#ifndef HELR_NTT_SMALL_GRID
+#define HELR_NTT_SMALL_GRID (2 * 148)
+#endif
+constexpr long long NTT_SMALL_GRID = HELR_NTT_SMALL_GRID;
+#ifndef HELR_NTT_SMALL_LOGR
+#define HELR_NTT_SMALL_LOGR 2
+#endif
 
 template <int LOG_T, bool IS_COL, bool INV, int S2, class Ld, class St>
 static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
@@ -576,9 +582,13 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
     if (cols == COLS) {
         const long long full = (long long)(subs / COLS) * map.count * count;
         if (COLS_S < COLS && full < NTT_SMALL_GRID && log_n >= 12) {
+            // small grids (single-ciphertext key switches, W/V updates) are
+            // latency-bound: quarter-size tiles, and radix-4 register groups
+            // so each tile has 4x the threads (more warps per SM in flight)
+            constexpr int LOG_RS = LOG_T >= 6 ? HELR_NTT_SMALL_LOGR : LOG_R;
             dim3 grid = ntt_grid(subs / COLS_S, map.count, count);
-            launch_pdl(ntt_pass<LOG_T, LOG_R, COLS_S, IS_COL, INV, S2, Ld, St>, grid, dim3(T * COLS_S / (1 << LOG_R)), 0, s, ld, st,
-                       tb, map, a);
+            launch_pdl(ntt_pass<LOG_T, LOG_RS, COLS_S, IS_COL, INV, S2, Ld, St>, grid,
+                       dim3(T * COLS_S / (1 << LOG_RS)), 0, s, ld, st, tb, map, a);
             return;
         }
         dim3 grid = ntt_grid(subs / COLS, map.count, count);
