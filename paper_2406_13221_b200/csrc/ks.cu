@@ -344,6 +344,8 @@ static int ks_modup(helr_ctx* c, KsInput in, int level, int B, const KsWs& w, cu
         ProfScope ps(PROF_MODUP, 8.0 * n * B * (2.0 * nl + (double)nd * ne), s);
         if (c->alpha <= 4) launch_pdl(k_modup<4>, g, dim3(128), 0, s, a, c->t);
         else if (c->alpha <= 8) launch_pdl(k_modup<8>, g, dim3(128), 0, s, a, c->t);
+        else if (c->alpha <= 16) launch_pdl(k_modup<16>, g, dim3(128), 0, s, a, c->t);
+        else if (c->alpha <= 32) launch_pdl(k_modup<32>, g, dim3(128), 0, s, a, c->t);
         else launch_pdl(k_modup<HELR_MAXP>, g, dim3(128), 0, s, a, c->t);
         CHECK_KERNEL("ks modup");
     }
@@ -398,7 +400,11 @@ static int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const
     dim3 g(blocks_for(n / 2, 128), 2 * B);
     {
         ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + nl), s);
-        auto conv = K <= 4 ? k_moddown_conv<4> : (K <= 8 ? k_moddown_conv<8> : k_moddown_conv<HELR_MAXP>);
+        // register arrays sized to K (dnum 1 rings have K up to ~31)
+        auto conv = K <= 4 ? k_moddown_conv<4>
+                  : K <= 8 ? k_moddown_conv<8>
+                  : K <= 16 ? k_moddown_conv<16>
+                  : K <= 32 ? k_moddown_conv<32> : k_moddown_conv<HELR_MAXP>;
         launch_pdl(conv, g, dim3(128), 0, s, (const u64*)w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv,
                    c->md_phinv_sh, c->md_phmod, c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
         CHECK_KERNEL("ks moddown conv");
@@ -569,7 +575,10 @@ static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, in
     {
         dim3 g(blocks_for(n / 2, 128), 2 * B);
         ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + 1 + l), s);
-        auto conv = K + 1 <= 4 ? k_mdr_conv<4> : (K + 1 <= 8 ? k_mdr_conv<8> : k_mdr_conv<HELR_MAXP>);
+        auto conv = K + 1 <= 4 ? k_mdr_conv<4>
+                  : K + 1 <= 8 ? k_mdr_conv<8>
+                  : K + 1 <= 16 ? k_mdr_conv<16>
+                  : K + 1 <= 32 ? k_mdr_conv<32> : k_mdr_conv<HELR_MAXP>;
         launch_pdl(conv, g, dim3(128), 0, s, (const u64*)w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, mt, c->t);
         CHECK_KERNEL("mdr conv");
     }
