@@ -178,7 +178,10 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
 }
 
 template <int ND, int NB>
-__global__ void __launch_bounds__(HOIST_T, 3) k_ks_inner_hoisted(HoistKeys hk, HoistArgs A, Tables tb) {
+#ifndef HELR_HOIST_MINB
+#define HELR_HOIST_MINB 3
+#endif
+__global__ void __launch_bounds__(HOIST_T, HELR_HOIST_MINB) k_ks_inner_hoisted(HoistKeys hk, HoistArgs A, Tables tb) {
     pdl_begin();
     const int e = blockIdx.y;
     const int p = e < A.nl ? e : A.L + (e - A.nl);
