@@ -153,6 +153,31 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
         }
     }
     cp_async_wait<0>();
+    if constexpr (DBL) {
+        // fold on the fp64 pipe (see k_ks_inner): hh 2^42 + mid 2^21 + ll
+        const DblC dc{tb.qd[p], tb.qinvd[p]};
+        const double t42 = reduce_d(4398046511104.0, dc);
+        auto fold = [&](const dacc& c) -> double {
+            return __dadd_rn(__dadd_rn(mulmod_d(reduce_d(c.hh, dc), t42, dc), mulmod_d(reduce_d(c.mid, dc), 2097152.0, dc)),
+                             reduce_d(c.ll, dc));
+        };
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            if (b < nb) {
+                u64* ap = acc + (size_t)(b0 + b) * acc_item_stride;
+                double f0 = fold(a0[b]), f1 = fold(a1[b]);
+                if (A.dadd && e < nl) {  // merged ModDown + rescale: + (P mod q) * (d0, d1)
+                    const u64* db = A.dadd + (size_t)(b0 + b) * A.dadd_is + (size_t)e * n + i;
+                    const double w = u2d(A.pm[e]);
+                    f0 = __dadd_rn(f0, mulmod_d(u2d(db[0]), w, dc));
+                    f1 = __dadd_rn(f1, mulmod_d(u2d(db[(size_t)L * n]), w, dc));
+                }
+                ap[(size_t)e * n + i] = d2u_canon(f0, dc);
+                ap[((size_t)(nl + K) + e) * n + i] = d2u_canon(f1, dc);
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int b = 0; b < NB; b++) {
         if (b < nb) {

@@ -181,10 +181,30 @@ __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long 
             mac_d(c10, uxh, uxl, k1xh, k1xl);
             mac_d(c11, uyh, uyl, k1yh, k1yl);
         }
-        o00 = reduce128(dresolve_s(c00), q, r1, r0, one_sh[p]);
-        o01 = reduce128(dresolve_s(c01), q, r1, r0, one_sh[p]);
-        o10 = reduce128(dresolve_s(c10), q, r1, r0, one_sh[p]);
-        o11 = reduce128(dresolve_s(c11), q, r1, r0, one_sh[p]);
+        // fold on the fp64 pipe (idle here; the integer 128-bit Barrett path
+        // was the kernel's bottleneck): hh 2^42 + mid 2^21 + ll, each part
+        // reduced first, plus the merged-rescale addend (P mod q) d
+        const DblC dc{tb.qd[p], tb.qinvd[p]};
+        const double t42 = reduce_d(4398046511104.0, dc);  // 2^42 mod q (signed)
+        const double t21 = 2097152.0;
+        auto fold = [&](const dacc& c) -> double {
+            return __dadd_rn(__dadd_rn(mulmod_d(reduce_d(c.hh, dc), t42, dc), mulmod_d(reduce_d(c.mid, dc), t21, dc)),
+                             reduce_d(c.ll, dc));
+        };
+        double f00 = fold(c00), f01 = fold(c01), f10 = fold(c10), f11 = fold(c11);
+        if (dadd && e < nl) {
+            const u64* db = dadd + (size_t)b * dadd_is + (size_t)e * n + i;
+            const ulonglong2 d0 = ld2(db), d1 = ld2(db + (size_t)L * n);
+            const double w = u2d(pm[e]);
+            f00 = __dadd_rn(f00, mulmod_d(u2d(d0.x), w, dc));
+            f01 = __dadd_rn(f01, mulmod_d(u2d(d0.y), w, dc));
+            f10 = __dadd_rn(f10, mulmod_d(u2d(d1.x), w, dc));
+            f11 = __dadd_rn(f11, mulmod_d(u2d(d1.y), w, dc));
+        }
+        u64* ap = acc + (size_t)b * acc_item_stride;
+        st2(ap + (size_t)e * n + i, d2u_canon(f00, dc), d2u_canon(f01, dc));
+        st2(ap + ((size_t)(nl + K) + e) * n + i, d2u_canon(f10, dc), d2u_canon(f11, dc));
+        return;
     } else {
     u128v a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
     for (int j = 0; j < nd; j++) {
