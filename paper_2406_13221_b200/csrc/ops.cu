@@ -30,11 +30,11 @@ struct EwGeom {
 };
 __device__ __forceinline__ void ew_decode(long long idx, const EwGeom& g, int& item, int& poly, int& limb, int& k) {
     k = (int)(idx & (g.n - 1));
-    long long r = idx >> g.log_n;
-    limb = (int)(r % g.nl);
-    r /= g.nl;
-    poly = (int)(r & 1);
-    item = (int)(r >> 1);
+    const unsigned r = (unsigned)(idx >> g.log_n);  // < items * 2 * limbs: 32-bit division
+    const unsigned rq = r / (unsigned)g.nl;
+    limb = (int)(r - rq * (unsigned)g.nl);
+    poly = (int)(rq & 1u);
+    item = (int)(rq >> 1);
 }
 
 
@@ -487,6 +487,22 @@ __global__ void k_lincomb(LinArgs la, u64* out, long long os, int n, int L, Tabl
     const int item = it >> 1, poly = it & 1;
     const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p];
     u64* op = out + (size_t)item * os + ((size_t)poly * L + p) * n;
+    if (q < NTT_DBL_BOUND) {  // fp64: exact signed products, one canonicalisation
+        const DblC dc{tb.qd[p], tb.qinvd[p]};
+        double kd[4];
+#pragma unroll
+        for (int t = 0; t < 4; t++) kd[t] = t < la.terms ? u2d(la.k[t][p]) : 0.0;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+            double acc = 0.0;
+#pragma unroll
+            for (int t = 0; t < 4; t++)
+                if (t < la.terms)
+                    acc = __dadd_rn(acc, mulmod_d(u2d(la.x[t][(size_t)item * la.xs[t] + ((size_t)poly * L + p) * n + i]),
+                                                  kd[t], dc));
+            op[i] = d2u_canon(acc, dc);
+        }
+        return;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         u128v acc{0, 0};
         for (int t = 0; t < la.terms; t++)
