@@ -448,6 +448,13 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                 }
             }
             if constexpr (!IS_COL && has_tile<St>::value) {
+                if (lo != 0) {
+                    // the last group spreads each thread over a stride of 2^lo:
+                    // consecutive threads of a block store consecutive words
+                    // (full segments), no shared-memory staging needed
+#pragma unroll
+                    for (int i = 0; i < R; i++) ST(base + (i << lo), y[i]);
+                } else {
                 if (NG > 1) __syncthreads();  // this group's shared-memory reads are done
 #pragma unroll
                 for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = y[i];
@@ -460,6 +467,7 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                     const u64 v0 = sm[c2 * SROW + k + (k >> 4)], v1 = sm[c2 * SROW + k + 1 + ((k + 1) >> 4)];
                     if constexpr (SP) *reinterpret_cast<ulonglong2*>(scta + e) = make_ulonglong2(v0, v1);
                     else st.store2(z, li, prime, ((bx * COLS + c2) << LOG_T) + k, make_ulonglong2(v0, v1));
+                }
                 }
             } else if constexpr (!IS_COL && has_vec<St>::value) {
                 if (lo == 0) {
