@@ -186,11 +186,30 @@ __device__ __forceinline__ double d2d_canon(double x, const DblC& c) {
     const double r = reduce_d(x, c);
     return r < 0.0 ? __dadd_rn(r, c.q) : r;
 }
+// A stage's R / 2^(H+1) twiddles are contiguous and, when there are two or
+// more, start at an even index (the low bits of the register group's base
+// are zero above bit lo), so they load as 16-byte pairs, all issued before
+// the butterflies.
+template <int NW>
+__device__ __forceinline__ void load_tw(double (&w)[NW], const double* __restrict__ W, int tb0) {
+    if constexpr (NW >= 2) {
+#pragma unroll
+        for (int j = 0; j < NW; j += 2) {
+            const double2 p = __ldg(reinterpret_cast<const double2*>(W + tb0 + j));
+            w[j] = p.x;
+            w[j + 1] = p.y;
+        }
+    } else {
+        w[0] = __ldg(W + tb0);
+    }
+}
 template <int R, int H>
 __device__ __forceinline__ void fwd_stage_d(double (&x)[R], const double* __restrict__ W, int tb0, const DblC& c) {
+    double wv[R >> (H + 1)];
+    load_tw(wv, W, tb0);
 #pragma unroll
     for (int j = 0; j < (R >> (H + 1)); j++) {
-        const double w = __ldg(W + tb0 + j);
+        const double w = wv[j];
 #pragma unroll
         for (int t = 0; t < (1 << H); t++) {
             const int i = (j << (H + 1)) + t;
@@ -202,9 +221,11 @@ __device__ __forceinline__ void fwd_stage_d(double (&x)[R], const double* __rest
 }
 template <int R, int H>
 __device__ __forceinline__ void inv_stage_d(double (&x)[R], const double* __restrict__ W, int tb0, const DblC& c) {
+    double wv[R >> (H + 1)];
+    load_tw(wv, W, tb0);
 #pragma unroll
     for (int j = 0; j < (R >> (H + 1)); j++) {
-        const double w = __ldg(W + tb0 + j);
+        const double w = wv[j];
 #pragma unroll
         for (int t = 0; t < (1 << H); t++) {
             const int i = (j << (H + 1)) + t;
