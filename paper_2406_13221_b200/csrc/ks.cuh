@@ -27,11 +27,14 @@ __device__ __forceinline__ int brv_dev(int x, int log_n) { return (int)(__brev((
 __device__ __forceinline__ ulonglong2 ld2(const u64* p) { return *reinterpret_cast<const ulonglong2*>(p); }
 __device__ __forceinline__ void st2(u64* p, u64 x, u64 y) { *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(x, y); }
 // NTT-slot permutation of X -> X^g: out[i] = in[perm(i)]
+// (2N is a power of two <= 2^17, so the product is needed only mod 2^32:
+// 32-bit arithmetic, one IMAD)
+__device__ __forceinline__ int galois_perm_e(unsigned e, u64 g, int log_n) {  // e = 2 brv(i) + 1
+    const unsigned f = (e * (unsigned)g) & ((2u << log_n) - 1u);
+    return brv_dev((int)((f - 1u) >> 1), log_n);
+}
 __device__ __forceinline__ int galois_perm(int i, u64 g, int log_n) {
-    const u64 two_n = 2ull << log_n;
-    const u64 e = 2ull * (u64)brv_dev(i, log_n) + 1ull;
-    const u64 f = (e * g) & (two_n - 1);
-    return brv_dev((int)((f - 1) >> 1), log_n);
+    return galois_perm_e(2u * (unsigned)brv_dev(i, log_n) + 1u, g, log_n);
 }
 
 
@@ -185,8 +188,9 @@ struct StCombine {
             // off is even, and a Galois permutation maps the pair (off, off + 1)
             // onto the aligned pair (s, s ^ 1): one index and one 16-byte load per step
             const u64* pp = add_p + (size_t)item * p_is + (size_t)p * n;
+            const unsigned eo = 2u * (unsigned)brv_dev(off, log_n) + 1u;
             for (int t = 0; t < ngal; t++) {
-                const int src = galois_perm(off, (u64)gal[t], log_n);
+                const int src = galois_perm_e(eo, (u64)gal[t], log_n);
                 const ulonglong2 pr = ld2(pp + (src & ~1));
                 r0 = add_mod(r0, (src & 1) ? pr.y : pr.x, qq);
                 r1 = add_mod(r1, (src & 1) ? pr.x : pr.y, qq);
