@@ -68,10 +68,11 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
     const size_t k1off = ((size_t)LK + p) * n + i;
     const size_t kds = (size_t)2 * LK * n;
     auto slot = [&](int stage, int w) -> u64* { return hsm + ((size_t)(stage * W + w) * HOIST_T + tid); };
+    const unsigned ei = 2u * (unsigned)brv_dev(i, log_n) + 1u;  // Galois index of this coefficient
     auto issue = [&](int t) {
         if (t < hk.nsteps) {
             const int stage = t % S;
-            const int src = galois_perm(i, (u64)hk.gal[t], log_n);
+            const int src = galois_perm_e(ei, (u64)hk.gal[t], log_n);
             const u64* kt = hk.key[t];
 #pragma unroll
             for (int j = 0; j < ND; j++) {
