@@ -590,6 +590,9 @@ struct StBuf {
 #define HELR_NTT_SMALL_GRID (2 * 148)
 #endif
 constexpr long long NTT_SMALL_GRID = HELR_NTT_SMALL_GRID;
+#ifndef HELR_NTT_COLS
+#define HELR_NTT_COLS 16  // adjacent columns per column-pass CTA (16 x 8 B = one 128-byte segment)
+#endif
 #ifndef HELR_NTT_SMALL_LOGR
 #define HELR_NTT_SMALL_LOGR 2
 #endif
@@ -602,7 +605,7 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
     constexpr int T = 1 << LOG_T;
     // column passes: 16 adjacent columns (128-byte rows); row passes: ~4096 elements per CTA
     constexpr int COLS_ROW = (4096 / T) > 0 ? (4096 / T) : 1;
-    constexpr int COLS = IS_COL ? 16 : COLS_ROW;
+    constexpr int COLS = IS_COL ? HELR_NTT_COLS : COLS_ROW;
     constexpr int COLS_S = COLS >= 4 ? COLS / 4 : 1;
     const int subs = IS_COL ? (1 << (log_n - LOG_T)) : (1 << (log_n - LOG_T));
     const int cols = subs < COLS ? subs : COLS;  // tiny rings: fewer sub-transforms than COLS

@@ -1,5 +1,5 @@
 # Build-time knob sweep on the GPU box: rebuild with each HELR_NVCC_DEFS and time 100 steps
-for defs in "" "-DHELR_NTT_SMALL_LOGR=1" "-DHELR_NTT_SMALL_GRID=592" "-DHELR_NTT_SMALL_GRID=1184"; do
+for defs in "-DHELR_NTT_COLS=8" "-DHELR_NTT_COLS=32" ""; do
   HELR_NVCC_DEFS="$defs" python -m paper_2406_13221_b200.build --force > /dev/null 2>&1 || { echo "build failed: $defs"; continue; }
   python bench.py --steps 100 --warmup 5 --no-e2e --cpu-iters 0 --profile-steps 1 > gpurun_out/knob.json 2>/dev/null
   python - "$defs" <<'PY'
