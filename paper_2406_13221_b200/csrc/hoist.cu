@@ -23,7 +23,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 constexpr int HOIST_T = 128;     // threads per block (coefficients per tile)
-constexpr int HOIST_STAGES = 3;  // steps in flight per thread
+#ifndef HELR_HOIST_STAGES
+#define HELR_HOIST_STAGES 3
+#endif
+constexpr int HOIST_STAGES = HELR_HOIST_STAGES;  // steps in flight per thread
 
 
 // grid: x = coefficient tile * chunks + chunk (chunks of NB ciphertexts share
