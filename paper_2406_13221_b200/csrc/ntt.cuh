@@ -28,6 +28,11 @@
 #include "ctx.cuh"
 #include "prof.cuh"
 
+#ifndef HELR_NTT_EPI_UNROLL
+#define HELR_NTT_EPI_UNROLL 4  // tile-epilogue pairs per thread in flight
+#endif
+constexpr int kNttEpiUnroll = HELR_NTT_EPI_UNROLL;
+
 void count_launches(int k);
 
 struct NttPassArgs {
@@ -482,7 +487,7 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                 __syncthreads();
                 constexpr int TOT = T * COLS;
                 const int nthr = T * COLS / R;
-#pragma unroll 4
+#pragma unroll (kNttEpiUnroll)
                 for (int e = 2 * tid; e < TOT; e += 2 * nthr) {
                     const int c2 = e >> LOG_T, k = e & (T - 1);
                     const u64 v0 = sm[c2 * SROW + k + (k >> 4)], v1 = sm[c2 * SROW + k + 1 + ((k + 1) >> 4)];
