@@ -127,13 +127,13 @@ int helr_add_plain(helr_ctx* ctx, const uint64_t* a, const uint64_t* pt,
 int helr_mul_const(helr_ctx* ctx, const uint64_t* a, const uint64_t* c,
                    uint64_t* out, int count, int level, void* stream);
 /* Both polynomials times an NTT plaintext; no rescale. */
+int helr_mul_plain(helr_ctx* ctx, const uint64_t* a, const uint64_t* pt,
+                   uint64_t* out, int count, int level, void* stream);
 /* Fold every residue word (any value < 2^64, e.g. the element-wise sum of up
  * to 8 ranks' residue vectors after an all-reduce) back to [0, q_i).  New:
  * the combine step of the sharded full-batch gradient; the
  * reference sums block gradients with SimContext.add (enctrain.py:374-381). */
 int helr_reduce(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count, int level, void* stream);
-int helr_mul_plain(helr_ctx* ctx, const uint64_t* a, const uint64_t* pt,
-                   uint64_t* out, int count, int level, void* stream);
 /* Drop q_level: out (level-1) = round(in / q_level). */
 int helr_rescale(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count,
                  int level, void* stream);
@@ -238,6 +238,9 @@ int helr_nag_iteration(helr_ctx* ctx, const helr_nag_args* args, void* stream);
 /* Capture / replay the iteration as a CUDA graph (same arguments each
  * replay; constants are read from args->consts at replay time). */
 int helr_nag_graph_capture(helr_ctx* ctx, const helr_nag_args* args, void* stream, void** graph_exec);
+/* Re-point a captured graph at new arguments of the same shape (another
+ * batch of the resident dataset) by re-capturing and updating it in place. */
+int helr_nag_graph_update(helr_ctx* ctx, const helr_nag_args* args, void* stream, void* graph_exec);
 int helr_nag_graph_launch(void* graph_exec, void* stream);
 int helr_nag_graph_destroy(void* graph_exec);
 

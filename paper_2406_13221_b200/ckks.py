@@ -32,6 +32,7 @@ log_delta == log_delta_c == scale_bits (see params.py).
 
 from __future__ import annotations
 
+import secrets
 import weakref
 from typing import Optional
 
@@ -40,14 +41,10 @@ import torch
 
 from . import _lib
 from .encoder import Encoder
+from .errors import NeedsBootstrap
 from .params import CkksParams
 
 __all__ = ["GpuContext", "GpuCiphertext", "NeedsBootstrap"]
-
-
-class NeedsBootstrap(Exception):
-    """Raised when an operation would leave too little modulus to decrypt
-    (mirrors helr.hesim.NeedsBootstrap, hesim.py:37-38)."""
 
 
 def _ptr(t: torch.Tensor) -> int:
@@ -90,12 +87,17 @@ class GpuContext:
 
     ``seed`` drives every random draw (secret key, switching keys,
     encryption randomness) through the counter-based generator shared with
-    the CPU oracle, so a given seed reproduces the same residues there.
+    the CPU ring checker, so a given seed reproduces the same residues there.
+    With ``seed=None`` (the default) the seed is drawn from the OS CSPRNG
+    (``secrets``).  An explicit seed is for reproducible parity runs only:
+    anyone who knows it can regenerate the secret key.  The counter generator
+    (SplitMix64) is not a cryptographic PRNG either — this engine is a
+    performance / parity vehicle, not a hardened HE library.
     """
 
     COUNTER_KEYS = ("enc", "dec", "add", "cadd", "mul", "cmul", "imul", "rotate", "bootstrap")
 
-    def __init__(self, ckks: CkksParams, seed: int = 0, noise_sigma: float = 1e-7,
+    def __init__(self, ckks: CkksParams, seed: Optional[int] = None, noise_sigma: float = 1e-7,
                  device: Optional[str] = None, max_batch: int = 8):
         if not torch.cuda.is_available():
             raise _lib.NativeLibraryError("GpuContext needs a CUDA device (no CPU fallback)")
@@ -103,7 +105,7 @@ class GpuContext:
         self.params = ckks.he_params(noise_sigma=noise_sigma, seed=seed)
         self.device = torch.device(device or "cuda")
         self.encoder = Encoder(ckks.log_n)
-        self.seed = int(seed)
+        self.seed = int(secrets.randbits(62)) if seed is None else int(seed)
         self.key_seed = (self.seed << 1) | 1
         self.enc_seed = (self.seed << 1) + 2
         self.counters = dict.fromkeys(self.COUNTER_KEYS, 0)

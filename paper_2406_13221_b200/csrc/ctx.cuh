@@ -74,6 +74,7 @@ struct helr_ctx {
     // fused-iteration driver workspace (nag.cu), allocated on first use
     u64* nag_ws = nullptr;
     size_t nag_words = 0;
+    int nag_graphs = 0;  // live captured graphs pointing into nag_ws
     // device encoder tables (encode.cu), built on first use
     void* enc_tw = nullptr;   // double2[N/2]
     int* enc_tpos = nullptr;  // [N/2]

@@ -26,22 +26,41 @@
     } while (0)
 
 // The driver workspace belongs to the context (like the key-switching
-// workspace): contexts used from different streams never share scratch.
-static int nag_buffers(helr_ctx* c, int rows, int cols, u64** out) {
+// workspace).  It only grows, and never while a captured graph that points
+// into it is alive (helr_nag_graph_capture / _destroy keep the count): a
+// reallocation would leave those graphs writing freed memory.  One fused
+// trainer per context at a time: trainers on different streams would race
+// on this scratch.
+static int nag_buffers(helr_ctx* c, int rows, int cols, cudaStream_t s, u64** out) {
     const size_t cs = 2ull * c->L * c->n;
     const size_t need = cs * (7ull * rows + 5ull * cols);
     if (c->nag_ws && c->nag_words >= need) { *out = c->nag_ws; return HELR_OK; }
     cudaStreamCaptureStatus st;
-    if (cudaStreamIsCapturing(0, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+    if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
         set_error("nag workspace must be allocated before graph capture (run one iteration first)");
         return HELR_EINVAL;
     }
-    if (c->nag_ws) { cudaFree(c->nag_ws); c->nag_ws = nullptr; c->nag_words = 0; }
+    if (c->nag_graphs > 0) {
+        set_error("nag workspace would grow while captured graphs still use it (destroy them first)");
+        return HELR_EINVAL;
+    }
+    if (c->nag_ws) {
+        cudaStreamSynchronize(s);
+        cudaFree(c->nag_ws);
+        c->nag_ws = nullptr;
+        c->nag_words = 0;
+    }
     if (!cuda_ok(cudaMalloc(&c->nag_ws, need * sizeof(u64)), "cudaMalloc(nag workspace)")) return HELR_ENOMEM;
     c->nag_words = need;
     *out = c->nag_ws;
     return HELR_OK;
 }
+
+// opaque graph handle returned to the host: the exec plus its context
+struct nag_graph {
+    cudaGraphExec_t exec;
+    helr_ctx* ctx;
+};
 
 static long long pow_mod_ll(long long b, long long e, long long m) {
     long long r = 1 % m;
@@ -112,7 +131,7 @@ static int nag_run(helr_ctx* c, const helr_nag_args* a, cudaStream_t s) {
     if (lw < 7 || lw >= L) { set_error("nag: lw must be in [7, L)"); return HELR_EINVAL; }
 
     u64* ws = nullptr;
-    TRY(nag_buffers(c, R, C, &ws));
+    TRY(nag_buffers(c, R, C, s, &ws));
     u64* T1 = ws;                        // [R] products before rescale
     u64* X0 = T1 + (size_t)R * CS;       // [R] ping
     u64* X1 = X0 + (size_t)R * CS;       // [R] pong
@@ -229,7 +248,7 @@ extern "C" int helr_nag_graph_capture(helr_ctx* c, const helr_nag_args* a, void*
     if (!c || !a || !graph_exec) { set_error("null argument"); return HELR_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
     u64* ws = nullptr;
-    TRY(nag_buffers(c, a->rows, a->cols, &ws));
+    TRY(nag_buffers(c, a->rows, a->cols, s, &ws));
     if (!cuda_ok(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture")) return HELR_ECUDA;
     int r = nag_run(c, a, s);
     cudaGraph_t graph = nullptr;
@@ -240,19 +259,56 @@ extern "C" int helr_nag_graph_capture(helr_ctx* c, const helr_nag_args* a, void*
     e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (!cuda_ok(e, "graph instantiate")) return HELR_ECUDA;
-    *graph_exec = (void*)exec;
+    nag_graph* h = new nag_graph{exec, c};
+    c->nag_graphs++;
+    *graph_exec = (void*)h;
+    return HELR_OK;
+}
+
+// Re-point a captured iteration at new arguments (a different batch of the
+// resident dataset, other constants) without a new instantiation: capture
+// the iteration again and update the executable graph in place (the
+// topology is identical for equal (rows, cols, lw, phase, group bits), so
+// cudaGraphExecUpdate only rewrites kernel parameters).  This replaces a
+// per-step device-to-device copy of the batch into fixed staging buffers.
+extern "C" int helr_nag_graph_update(helr_ctx* c, const helr_nag_args* a, void* stream, void* graph_exec) {
+    clear_stale_error("helr_nag_graph_update");
+    if (!c || !a || !graph_exec) { set_error("null argument"); return HELR_EINVAL; }
+    nag_graph* h = (nag_graph*)graph_exec;
+    if (h->ctx != c) { set_error("graph belongs to another context"); return HELR_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!cuda_ok(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture")) return HELR_ECUDA;
+    int r = nag_run(c, a, s);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (r) { if (graph) cudaGraphDestroy(graph); return r; }
+    if (!cuda_ok(e, "end capture")) return HELR_ECUDA;
+    cudaGraphExecUpdateResultInfo info;
+    e = cudaGraphExecUpdate(h->exec, graph, &info);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("graph update failed: topology changed");
+        return HELR_EINVAL;
+    }
     return HELR_OK;
 }
 
 extern "C" int helr_nag_graph_launch(void* graph_exec, void* stream) {
     clear_stale_error("helr_nag_graph_launch");
     if (!graph_exec) { set_error("null graph"); return HELR_EINVAL; }
-    if (!cuda_ok(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream), "graph launch")) return HELR_ECUDA;
+    nag_graph* h = (nag_graph*)graph_exec;
+    if (!cuda_ok(cudaGraphLaunch(h->exec, (cudaStream_t)stream), "graph launch")) return HELR_ECUDA;
     return HELR_OK;
 }
 
 extern "C" int helr_nag_graph_destroy(void* graph_exec) {
     clear_stale_error("helr_nag_graph_destroy");
-    if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+    if (graph_exec) {
+        nag_graph* h = (nag_graph*)graph_exec;
+        cudaGraphExecDestroy(h->exec);
+        if (h->ctx && h->ctx->nag_graphs > 0) h->ctx->nag_graphs--;
+        delete h;
+    }
     return HELR_OK;
 }

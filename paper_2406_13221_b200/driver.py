@@ -82,6 +82,8 @@ def _bind(lib):
     lib.helr_nag_graph_capture.argtypes = [ctypes.c_void_p, ctypes.POINTER(NagArgs), ctypes.c_void_p,
                                            ctypes.POINTER(ctypes.c_void_p)]
     lib.helr_nag_graph_capture.restype = ctypes.c_int
+    lib.helr_nag_graph_update.argtypes = [ctypes.c_void_p, ctypes.POINTER(NagArgs), ctypes.c_void_p, ctypes.c_void_p]
+    lib.helr_nag_graph_update.restype = ctypes.c_int
     lib.helr_nag_graph_launch.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     lib.helr_nag_graph_launch.restype = ctypes.c_int
     lib.helr_nag_graph_destroy.argtypes = [ctypes.c_void_p]
@@ -94,7 +96,7 @@ def _bind(lib):
 class IterPlan:
     lw: int
     consts: np.ndarray          # uint64 [NCONST][L]
-    ints: list                  # the signed integer constants (for the oracle)
+    ints: list                  # the signed integer constants (host-side record)
     mask_scale: float
     s_out: float
     scales: dict = field(default_factory=dict)
@@ -171,10 +173,10 @@ class FusedTrainer:
     per iteration in order; full-batch mode sums every batch's gradient
     before one B̄ product and update (enctrain.py:356-359, 374-381).
 
-    Every iteration reads its batch from fixed staging buffers (filled by a
-    device-to-device copy from the HBM-resident encrypted dataset, or by a
-    host-to-device copy when ``host_stream`` is set), so one captured CUDA
-    graph per phase serves every batch.
+    Every iteration reads its batch in place from the HBM-resident
+    encrypted dataset (one captured CUDA graph per phase, re-pointed at the
+    next batch with ``helr_nag_graph_update``), or, when ``host_stream`` is
+    set, from two staging buffers filled by host-to-device copies.
     """
 
     def __init__(self, ctx: GpuContext, ds, rows_per_block: int, blocks_per_batch: int = 1,
@@ -320,8 +322,6 @@ class FusedTrainer:
         self._cev = [None] * len(self._cring)
         self._ci = 0
         self.grad = torch.empty((C, 2, L, N), dtype=torch.int64, device=ctx.device)
-        self.zstage = torch.empty((R, C, 2, L, N), dtype=torch.int64, device=ctx.device)
-        self.bstage = torch.empty((C, 2, L, N), dtype=torch.int64, device=ctx.device)
         self.w_host = torch.empty((2 * C, 2, L, N), dtype=torch.int64).pin_memory()
         torch.cuda.synchronize()
         self.timings["prepare_s"] = time.perf_counter() - t0
@@ -341,8 +341,8 @@ class FusedTrainer:
             self.b_host.copy_(self.bbar)
         if self.copy_stream is None:
             self.copy_stream = torch.cuda.Stream(device=self.ctx.device)
-            self._zst = [self.zstage, torch.empty_like(self.zstage)]
-            self._bst = [self.bstage, torch.empty_like(self.bstage)]
+            self._zst = [torch.empty_like(self.z[0]) for _ in range(2)]
+            self._bst = [torch.empty_like(self.bbar[0]) for _ in range(2)]
             self.w_snap = torch.empty_like(self.wv)
         self._d2h_ev = None
         self._buf = 0
@@ -404,10 +404,10 @@ class FusedTrainer:
         self.level = top
         self.s_w = self.s_v = target
 
-    def _args(self, plan: IterPlan, phase: int, zb=None) -> NagArgs:
+    def _args(self, plan: IterPlan, phase: int, zb) -> NagArgs:
         C = self.cols
         cs = self.wv[0].numel() * 8
-        z_ptr, b_ptr = zb if zb is not None else (self.zstage.data_ptr(), self.bstage.data_ptr())
+        z_ptr, b_ptr = zb
         return NagArgs(z=z_ptr, rows=self.rows, cols=C, log_g=self.log_g, log_m=self.log_m,
                        w=self.wv.data_ptr(), v=self.wv.data_ptr() + C * cs, bbar=b_ptr,
                        lw=plan.lw, rlk=self.ctx.rlk.data_ptr(), rot_left=self._k_left, rot_right=self._k_right,
@@ -431,10 +431,9 @@ class FusedTrainer:
         """Make (batch, bbar_index) resident in a staging buffer; returns the
         (z, bbar) device pointers the iteration reads."""
         if not self.host_stream:
-            self.zstage.copy_(self.z[batch], non_blocking=True)
-            if with_bbar:
-                self.bstage.copy_(self.bbar[bbar_index], non_blocking=True)
-            return self.zstage.data_ptr(), self.bstage.data_ptr()
+            # resident dataset: the iteration reads the batch in place (a
+            # captured graph is re-pointed with helr_nag_graph_update)
+            return self.z[batch].data_ptr(), self.bbar[bbar_index].data_ptr()
         buf = self._buf
         if self._loaded[buf] is None or self._loaded[buf][0] != batch or self._loaded[buf][1] != bbar_index:
             self._prefetch(buf, batch, bbar_index)
@@ -472,14 +471,21 @@ class FusedTrainer:
             _lib.check(self.lib.helr_nag_iteration(self.ctx.handle, ctypes.byref(args), stream), "helr_nag_iteration")
             self._warm = True
             return
-        key = (args.lw, args.phase, args.mask_pt, args.z, args.bbar)
-        g = self._graphs.get(key)
-        if g is None:
+        # host-streamed batches alternate between two staging buffers: one
+        # graph each; resident batches share one graph re-pointed per step
+        ptrs = (args.z, args.bbar)
+        key = (args.lw, args.phase, args.mask_pt) + (ptrs if self.host_stream else ())
+        ent = self._graphs.get(key)
+        if ent is None:
             g = ctypes.c_void_p()
             _lib.check(self.lib.helr_nag_graph_capture(self.ctx.handle, ctypes.byref(args), stream, ctypes.byref(g)),
                        "helr_nag_graph_capture")
-            self._graphs[key] = g
-        _lib.check(self.lib.helr_nag_graph_launch(g, stream), "helr_nag_graph_launch")
+            ent = self._graphs[key] = [g, ptrs]
+        elif ent[1] != ptrs:
+            _lib.check(self.lib.helr_nag_graph_update(self.ctx.handle, ctypes.byref(args), stream, ent[0]),
+                       "helr_nag_graph_update")
+            ent[1] = ptrs
+        _lib.check(self.lib.helr_nag_graph_launch(ent[0], stream), "helr_nag_graph_launch")
 
     def profile_iteration(self, batch: Optional[int] = None) -> dict:
         """One iteration replayed from a freshly captured graph whose kernels are
@@ -495,7 +501,7 @@ class FusedTrainer:
             info = self.iterate(batch)
         finally:
             lib.helr_prof_enable(0)
-            for g in self._graphs.values():
+            for g, _ in self._graphs.values():
                 torch.cuda.synchronize()
                 lib.helr_nag_graph_destroy(g)
             self._graphs, self.use_graph, self._warm = saved, use, warm
@@ -612,6 +618,7 @@ class FusedTrainer:
         return np.concatenate(segs)[: lay.cols]
 
     def close(self):
-        for g in self._graphs.values():
+        torch.cuda.synchronize(self.ctx.device)
+        for g, _ in self._graphs.values():
             self.lib.helr_nag_graph_destroy(g)
         self._graphs.clear()

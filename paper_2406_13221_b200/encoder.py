@@ -12,7 +12,7 @@ The transform is one length-N complex FFT: with b_i = m_i * zeta^i,
 m(zeta^(2t+1)) = sum_i b_i exp(2 pi i t i / N), i.e. the evaluations are
 N * ifft(b).  Encoding and decoding stay on the host in fp64 (the device
 never sees floating point except in the refresh stand-in's ratio), so the
-device library and the CPU oracle are fed identical integers.
+device library and any CPU checker are fed identical integers.
 """
 
 from __future__ import annotations

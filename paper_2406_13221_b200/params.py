@@ -14,7 +14,7 @@ switching with ``dnum`` digits of ``alpha`` limbs, and one primitive 2N-th
 root of unity per prime.
 All primes are below 2**61 so the lazy [0, 8q) NTT butterflies (approximate
 Shoup quotients) and the 128-bit key-product accumulators never overflow.  Everything here is plain integer arithmetic and
-deterministic, so the device library and the CPU oracle are handed the
+deterministic, so the device library and any CPU checker are handed the
 identical chain and roots.
 
 Level accounting for the drop-in surface: a ciphertext whose top active

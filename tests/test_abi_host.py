@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 def test_binding_table_covers_header():
     names = set(declared_symbols())
     bound = set(_lib.SIGNATURES)
-    extra = {"helr_nag_graph_capture", "helr_nag_graph_launch", "helr_nag_graph_destroy", "helr_prof_enable",
+    extra = {"helr_nag_graph_capture", "helr_nag_graph_update", "helr_nag_graph_launch", "helr_nag_graph_destroy", "helr_prof_enable",
              "helr_prof_collect", "helr_launch_count"}
     assert names - bound <= extra
 
