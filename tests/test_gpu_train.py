@@ -3,6 +3,7 @@ stand-in every iteration) against golden weight traces produced by the
 REFERENCE simulator (tests/golden, tools/make_goldens.py).  BASELINE bar:
 decrypted weights and AUC within 1e-6 absolute."""
 
+import gc
 import math
 
 import numpy as np
@@ -22,12 +23,15 @@ GOLD = Path(__file__).resolve().parent / "golden"
 TOL = 1e-6
 
 
-def _run(name, ds, log_n, rows, blocks, mode, n_iters, use_graph=False, dnum=2):
+def _run(name, ds, log_n, rows, blocks, mode, n_iters=None, use_graph=True, dnum=2, seed=2):
+    """Worst |dw| and |dAUC| over every golden-recorded iteration up to
+    n_iters (None: the whole run the golden file covers)."""
     gold = np.load(GOLD / f"{name}.npz")
     ck = CkksParams.generate(log_n=log_n, n_q=8, dnum=dnum)
-    ctx = GpuContext(ck, seed=2, max_batch=8)
+    ctx = GpuContext(ck, seed=seed, max_batch=8)
     tr = FusedTrainer(ctx, ds, rows_per_block=rows, blocks_per_batch=blocks, mode=mode, use_graph=use_graph)
-    its = list(gold["iterations"])
+    its = [int(t) for t in gold["iterations"]]
+    n_iters = its[-1] if n_iters is None else n_iters
     worst_w, worst_auc = 0.0, 0.0
     for t in range(1, n_iters + 1):
         tr.iterate()
@@ -37,29 +41,48 @@ def _run(name, ds, log_n, rows, blocks, mode, n_iters, use_graph=False, dnum=2):
             worst_w = max(worst_w, float(np.max(np.abs(w - gold["weights"][k]))))
             worst_auc = max(worst_auc, abs(auroc(ds.y, ds.X @ w) - float(gold["auc"][k])))
     tr.close()
+    del tr, ctx
+    gc.collect()
+    torch.cuda.empty_cache()
     return worst_w, worst_auc
 
 
+@pytest.fixture(scope="module")
+def paper_ds():
+    return data.paper_dataset()
+
+
 def test_toy_all_iterations():
-    w, a = _run("toy", data.toy_dataset(), 13, 128, 1, "mini_batch", 24)
+    w, a = _run("toy", data.toy_dataset(), 13, 128, 1, "mini_batch", use_graph=False)
     print(f"toy: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
     assert w < TOL and a < TOL
 
 
 def test_toy_with_cuda_graph():
-    w, a = _run("toy", data.toy_dataset(), 13, 128, 1, "mini_batch", 24, use_graph=True, dnum=3)
+    w, a = _run("toy", data.toy_dataset(), 13, 128, 1, "mini_batch", use_graph=True, dnum=3)
     assert w < TOL and a < TOL
 
 
-def test_medium_first_iterations():
-    w, a = _run("medium", data.medium_dataset(), 15, 1024, 1, "mini_batch", 32)
-    print(f"medium: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
+def test_medium_whole_run():
+    """Medium: all 320 iterations (5 epochs)."""
+    w, a = _run("medium", data.medium_dataset(), 15, 1024, 1, "mini_batch")
+    print(f"medium 320 it: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
     assert w < TOL and a < TOL
 
 
-def test_paper_mini_first_iterations():
-    w, a = _run("paper_mini", data.paper_dataset(), 16, 128, 8, "mini_batch", 16, use_graph=True)
-    print(f"paper_mini: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
+@pytest.mark.parametrize("seed", [2, 3, 4])
+def test_paper_mini_whole_run(paper_ds, seed):
+    """Paper shape, mini-batch: all 1,239 iterations (3 epochs), three
+    key / noise seeds."""
+    w, a = _run("paper_mini", paper_ds, 16, 128, 8, "mini_batch", seed=seed)
+    print(f"paper_mini 1239 it seed {seed}: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
+    assert w < TOL and a < TOL
+
+
+def test_paper_full_whole_run(paper_ds):
+    """Paper shape, full-batch: all 10 iterations over the 3,304 ciphertexts."""
+    w, a = _run("paper_full", paper_ds, 16, 128, 8, "full_batch")
+    print(f"paper_full 10 it: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
     assert w < TOL and a < TOL
 
 
