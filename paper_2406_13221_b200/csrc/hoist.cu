@@ -220,6 +220,233 @@ __global__ void __launch_bounds__(HOIST_T, HELR_HOIST_MINB) k_ks_inner_hoisted(H
         hoist_body<ND, NB, false>(hk, A, tb);
 }
 
+// ---- bulk-copy pipeline variant ---------------------------------------------
+// One producer warp streams each rotation step's operands into a ring of
+// shared-memory stages with cp.async.bulk (completion on per-stage
+// mbarriers): the 2 * ND contiguous 1 KB key rows of the CTA's 128
+// coefficients, and for every (ciphertext, digit) the four 256-byte runs the
+// Galois permutation sends the CTA's four 32-coefficient warps to (a
+// permutation maps every 32-aligned run of NTT slots onto one 32-aligned
+// run).  The four consumer warps read their permuted digit words and key
+// words from shared memory and run the same multiply-accumulate and fold as
+// hoist_body; after each step every warp releases the stage on an "empty"
+// mbarrier.  Replaces 12 per-thread 8-byte cp.async per step with ~36 bulk
+// copies per CTA (HELR_HOIST_PIPE=0 keeps the per-thread kernel).
+#ifndef HELR_HOIST_PSTAGES
+#define HELR_HOIST_PSTAGES 4
+#endif
+constexpr int HP_S = HELR_HOIST_PSTAGES;
+constexpr int HP_C = 128;       // consumer threads = coefficients per CTA tile
+constexpr int HP_THREADS = HP_C + 32;
+
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int ND, int NB, bool DBL>
+__device__ __forceinline__ void hoist_pipe_body(const HoistKeys& hk, const HoistArgs& A, const Tables& tb, u64* sm,
+                                                u64* full, u64* empty) {
+    constexpr int KW = 2 * ND * HP_C;     // key words per stage
+    constexpr int DW = NB * ND * HP_C;    // digit words per stage
+    constexpr int SW = KW + DW;
+    const int n = A.n, log_n = A.log_n, nl = A.nl, K = A.K, L = A.L, LK = A.LK, B = A.B, nchunks = A.nchunks;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int e = blockIdx.y;
+    const int tile = blockIdx.x / nchunks, chunk = blockIdx.x - tile * nchunks;
+    const int i0 = tile * HP_C;
+    const int b0 = chunk * NB;
+    const int nb = B - b0 < NB ? B - b0 : NB;
+    const int p = e < nl ? e : L + (e - nl);
+    const size_t kds = (size_t)2 * LK * n;
+    const int nsteps = hk.nsteps;
+
+    if (warp == HP_C / 32) {
+        // ---------------- producer warp
+        const u64* xb = A.ext + (size_t)b0 * A.ext_item_stride + (size_t)e * n;
+        const unsigned bytes = (unsigned)(KW + nb * ND * HP_C) * 8u;
+        for (int t = 0; t < nsteps; t++) {
+            const int st = t % HP_S;
+            if (t >= HP_S) mbar_wait(&empty[st], (unsigned)((t / HP_S - 1) & 1));
+            if (lane == 0) mbar_expect_tx(&full[st], bytes);
+            __syncwarp();
+            u64* sb = sm + (size_t)st * SW;
+            const u64* kt = hk.key[t];
+            // copy c: c < 2 ND -> key row (poly, j); else digit run (b, j, w)
+            const int ncopies = 2 * ND + nb * ND * 4;
+            for (int c = lane; c < ncopies; c += 32) {
+                if (c < 2 * ND) {
+                    const int poly = c / ND, j = c % ND;
+                    bulk_g2s(sb + c * HP_C, kt + (size_t)j * kds + ((size_t)poly * LK + p) * n + i0, HP_C * 8, &full[st]);
+                } else {
+                    const int d = c - 2 * ND;
+                    const int w = d & 3, bj = d >> 2;       // bj = b * ND + j
+                    const int b = bj / ND, j = bj % ND;
+                    const int run = galois_perm(i0 + 32 * w, (u64)hk.gal[t], log_n) >> 5;
+                    bulk_g2s(sb + KW + (size_t)d * 32,
+                             xb + (size_t)b * A.ext_item_stride + (size_t)j * A.ext_digit_stride + (size_t)run * 32, 256,
+                             &full[st]);
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumer warps: one coefficient per thread
+    const int i = i0 + tid;
+    const u64 q = tb.q[p], r1 = tb.br1[p], r0 = tb.br0[p], osh = A.one_sh[p];
+    const unsigned ei = 2u * (unsigned)brv_dev(i, log_n) + 1u;
+    using Acc = typename std::conditional<DBL, dacc, macc>::type;
+    Acc a0[NB], a1[NB];
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        if constexpr (DBL) a0[b] = a1[b] = dacc{0.0, 0.0, 0.0};
+        else a0[b] = a1[b] = macc{0, 0, 0, 0};
+    }
+    int run = 0;
+    for (int t = 0; t < nsteps; t++) {
+        const int st = t % HP_S;
+        const int off = galois_perm_e(ei, (u64)hk.gal[t], log_n) & 31;
+        mbar_wait(&full[st], (unsigned)((t / HP_S) & 1));
+        const u64* sb = sm + (size_t)st * SW;
+        const u64* db = sb + KW + warp * 32 + off;   // + (b * ND + j) * 128
+        if constexpr (DBL) {
+            double k0h[ND], k0l[ND], k1h[ND], k1l[ND];
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                split21(sb[j * HP_C + tid], k0h[j], k0l[j]);
+                split21(sb[(ND + j) * HP_C + tid], k1h[j], k1l[j]);
+            }
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                if (b < nb) {
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        double uh, ul;
+                        split21_d(__longlong_as_double((long long)db[(b * ND + j) * HP_C]), uh, ul);
+                        mac_d(a0[b], uh, ul, k0h[j], k0l[j]);
+                        mac_d(a1[b], uh, ul, k1h[j], k1l[j]);
+                    }
+                }
+            }
+        } else {
+            if (run == A.fold) {
+#pragma unroll
+                for (int b = 0; b < NB; b++) {
+                    a0[b] = macc{reduce128(resolve(a0[b]), q, r1, r0, osh), 0, 0, 0};
+                    a1[b] = macc{reduce128(resolve(a1[b]), q, r1, r0, osh), 0, 0, 0};
+                }
+                run = 0;
+            }
+            run++;
+            u64 k0[ND], k1[ND];
+#pragma unroll
+            for (int j = 0; j < ND; j++) {
+                k0[j] = sb[j * HP_C + tid];
+                k1[j] = sb[(ND + j) * HP_C + tid];
+            }
+#pragma unroll
+            for (int b = 0; b < NB; b++) {
+                if (b < nb) {
+#pragma unroll
+                    for (int j = 0; j < ND; j++) {
+                        const u64 u = db[(b * ND + j) * HP_C];
+                        mac_split(a0[b], u, k0[j]);
+                        mac_split(a1[b], u, k1[j]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    u64* acc = A.acc;
+    if (i >= n) return;
+    if constexpr (DBL) {
+        const DblC dc{tb.qd[p], tb.qinvd[p]};
+        const double t42 = reduce_d(4398046511104.0, dc);
+        auto fold = [&](const dacc& c) -> double {
+            return __dadd_rn(__dadd_rn(mulmod_d(reduce_d(c.hh, dc), t42, dc), mulmod_d(reduce_d(c.mid, dc), 2097152.0, dc)),
+                             reduce_d(c.ll, dc));
+        };
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            if (b < nb) {
+                u64* ap = acc + (size_t)(b0 + b) * A.acc_item_stride;
+                double f0 = fold(a0[b]), f1 = fold(a1[b]);
+                if (A.dadd && e < nl) {
+                    const u64* dd = A.dadd + (size_t)(b0 + b) * A.dadd_is + (size_t)e * n + i;
+                    const double w = u2d(A.pm[e]);
+                    f0 = __dadd_rn(f0, mulmod_d(u2d(dd[0]), w, dc));
+                    f1 = __dadd_rn(f1, mulmod_d(u2d(dd[(size_t)L * n]), w, dc));
+                }
+                ap[(size_t)e * n + i] = d2u_canon(f0, dc);
+                ap[((size_t)(nl + K) + e) * n + i] = d2u_canon(f1, dc);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            if (b < nb) {
+                u64* ap = acc + (size_t)(b0 + b) * A.acc_item_stride;
+                u64 o0 = reduce128(resolve(a0[b]), q, r1, r0, osh);
+                u64 o1 = reduce128(resolve(a1[b]), q, r1, r0, osh);
+                if (A.dadd && e < nl) {
+                    const u64* dd = A.dadd + (size_t)(b0 + b) * A.dadd_is + (size_t)e * n + i;
+                    const u64 w = A.pm[e], ws = A.pm_sh[e];
+                    o0 = add_mod(o0, shoup(dd[0], w, ws, q), q);
+                    o1 = add_mod(o1, shoup(dd[(size_t)L * n], w, ws, q), q);
+                }
+                ap[(size_t)e * n + i] = o0;
+                ap[((size_t)(nl + K) + e) * n + i] = o1;
+            }
+        }
+    }
+}
+
+#ifndef HELR_HOIST_PMINB
+#define HELR_HOIST_PMINB 4
+#endif
+template <int ND, int NB>
+__global__ void __launch_bounds__(HP_THREADS, HELR_HOIST_PMINB) k_ks_inner_pipe(HoistKeys hk, HoistArgs A, Tables tb) {
+    extern __shared__ __align__(128) u64 hp_sm[];
+    __shared__ __align__(8) u64 bars[2 * HP_S];
+    pdl_begin();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < HP_S; s++) {
+            mbar_init(&bars[s], 1);                 // full: the producer's expect_tx arrival
+            mbar_init(&bars[HP_S + s], HP_C / 32);  // empty: one arrival per consumer warp
+        }
+    }
+    __syncthreads();
+    const int e = blockIdx.y;
+    const int p = e < A.nl ? e : A.L + (e - A.nl);
+    if (tb.q[p] < NTT_DBL_BOUND)  // uniform per CTA
+        hoist_pipe_body<ND, NB, true>(hk, A, tb, hp_sm, bars, bars + HP_S);
+    else
+        hoist_pipe_body<ND, NB, false>(hk, A, tb, hp_sm, bars, bars + HP_S);
+}
+
+static bool hoist_pipe_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* v = getenv("HELR_HOIST_PIPE");
+        on = v ? (atoi(v) != 0) : 0;  // measured slower: per-lane bulk copies serialise
+    }
+    return on != 0;
+}
+
+template <int ND, int NB>
+static void launch_pipe_nb(dim3 g, cudaStream_t s, const HoistKeys& hk, HoistArgs A, const Tables& tb) {
+    A.nchunks = (A.B + NB - 1) / NB;
+    const size_t smem = sizeof(u64) * (size_t)HP_S * (2 * ND + NB * ND) * HP_C;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ks_inner_pipe<ND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    g.x = (unsigned)(((A.n + HP_C - 1) / HP_C) * A.nchunks);
+    launch_pdl(k_ks_inner_pipe<ND, NB>, g, dim3(HP_THREADS), smem, s, hk, A, tb);
+}
+
 // Steps per 128-bit accumulation run: a run adds fold*nd products (each <
 // 2^(2 bits)) to a residue (< 2^bits) and must stay below 2^128.
 static int hoist_fold(const helr_ctx* c, int nd) {
@@ -262,6 +489,14 @@ static void launch_hoisted(dim3 g, cudaStream_t s, const HoistKeys& hk, const Ho
     const int cap = hoist_nb_cap();
     const int want = nb <= 1 ? 1 : nb <= 2 ? 2 : nb <= 4 ? 4 : 8;
     const int NBs = want < cap ? want : cap;
+    if (hoist_pipe_enabled() && A.n % HP_C == 0 && A.n >= 1024) {
+        if constexpr (ND <= 4) {
+            if (NBs == 1) { launch_pipe_nb<ND, 1>(g, s, hk, A, tb); return; }
+            if (NBs == 2) { launch_pipe_nb<ND, 2>(g, s, hk, A, tb); return; }
+            launch_pipe_nb<ND, 4>(g, s, hk, A, tb);
+            return;
+        }
+    }
     if (NBs == 1) launch_hoisted_nb<ND, 1>(g, s, hk, A, tb);
     else if (NBs == 2) launch_hoisted_nb<ND, 2>(g, s, hk, A, tb);
     else if (NBs == 4) launch_hoisted_nb<ND, 4>(g, s, hk, A, tb);
@@ -278,7 +513,10 @@ int key_inner(helr_ctx* c, const KsWs& w, const HoistKeys& hk, int nb, int level
     dim3 g(blocks_for(n, HOIST_T), ne, 1);
     HoistArgs A{w.ext, w.ext_s, w.ext_ds, w.acc, w.acc_s, n, c->log_n, nl, K, c->L, c->LK, nb, 1, hoist_fold(c, nd),
                 c->one_sh, dadd, dadd_is, c->pmod, c->pmod_sh};
-    ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne * hk.nsteps + 2.0 * nd * ne * hk.nsteps + 2.0 * nb * ne +
+    // algorithmic bytes: every operand once — the ModUp'd
+    // digits once (the per-step Galois gathers re-read them from L2), every
+    // step's key, the two output polynomials
+    ProfScope ps(PROF_INNER, 8.0 * n * ((double)nb * nd * ne + 2.0 * nd * ne * hk.nsteps + 2.0 * nb * ne +
                                         (dadd ? 2.0 * nb * nl : 0.0)), s);
     switch (nd) {
         case 1: launch_hoisted<1>(g, s, hk, A, c->t); break;

@@ -199,6 +199,14 @@ struct StCombine {
         st2(out + (size_t)item * out_is + (size_t)poly * out_ps + (size_t)p * n + off, r0, r1);
     }
 };
+// byte model of a StCombine last pass: per output limb the ModDown input x,
+// the optional addend, and (poly 0 only) the sigma-gathered c0 limb, each once
+inline double ntt_extra_words(const StCombine& st, const LimbMap& m, int count) {
+    double poly0 = 0.0;
+    if (st.per_poly > 0) poly0 = (double)(m.count < st.per_poly ? m.count : st.per_poly) * count;
+    else poly0 = (double)m.count * (count / 2.0);
+    return (double)m.count * count * (1.0 + (st.add_a ? 1.0 : 0.0)) + (st.add_p ? poly0 : 0.0);
+}
 static inline StCombine st_combine(const helr_ctx* c, u64* out, long long out_is, long long out_ps, const u64* x, long long x_is,
                             long long x_ps, const u64* w, const u64* wsh, int per_poly) {
     StCombine f;

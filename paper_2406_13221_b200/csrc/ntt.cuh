@@ -685,13 +685,27 @@ static void ntt_row(int lt, int log_n, const Ld& ld, const St& st, const Tables&
 
 inline int ntt_split_s1(int log_n) { return log_n / 2; }
 
+// limbs a fused storer reads besides the transform's own input (byte model);
+// overloaded for StCombine in ks.cuh
+template <class St>
+inline double ntt_extra_words(const St&, const LimbMap&, int) { return 0.0; }
+
+#include "ntt_cluster.cuh"
+
+
 template <bool INV, class Ld, class St>
 // in_raw: fp64 limbs arrive as raw integer-valued doubles (|x| < 2^50);
 // out_dbl: fp64 limbs leave as canonical residues stored as exact doubles
 static void ntt_launch(const helr_ctx* c, const Ld& ld, const St& st, u64* mid, long long mid_stride,
                        const LimbMap& map, int count, cudaStream_t s, int in_raw = 0, int out_dbl = 0) {
     const int log_n = c->log_n;
-    ProfScope ps(PROF_NTT, 16.0 * c->n * map.count * count, s);
+    // algorithmic bytes: every limb read and written once, plus the extra
+    // operands a fused storer reads once (StCombine: ntt_extra_words)
+    ProfScope ps(PROF_NTT, 8.0 * c->n * (2.0 * map.count * count + ntt_extra_words(st, map, count)), s);
+    if (log_n == ncl::LOG_N && ntt_cluster_enabled((long long)map.count * count)) {
+        ntt_cluster_launch<INV>(ld, st, c->t, map, count, s, in_raw, out_dbl);
+        return;
+    }
     if (log_n <= 11) {
         ntt_single<INV>(log_n, ld, st, c->t, map, count, s, in_raw, out_dbl);
         return;

@@ -45,6 +45,40 @@ bool pdl_enabled() {
     return on != 0;
 }
 
+// single-pass cluster NTT for N = 2^16 (ntt_cluster.cuh): HELR_NTT_CLUSTER=0
+// falls back to the two-pass kernels; HELR_NTT_CL_MIN = fewest limb
+// transforms per launch that take the cluster path
+bool ntt_cluster_enabled(long long limb_transforms) {
+    static int on = -1;
+    static long long lo = 1;
+    if (on < 0) {
+        const char* e = getenv("HELR_NTT_CLUSTER");
+        on = e ? (atoi(e) != 0) : 0;  // measured slower than the two-pass kernels
+        const char* m = getenv("HELR_NTT_CL_MIN");
+        lo = m ? atoll(m) : 1;
+    }
+    return on != 0 && limb_transforms >= lo;
+}
+// cp.async.bulk for the dense tile of the cluster NTT (HELR_NTT_BULK=0: plain loads / stores)
+bool ntt_bulk_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("HELR_NTT_BULK");
+        on = e ? (atoi(e) != 0) : 1;
+    }
+    return on != 0;
+}
+
+// cluster NTT exchange through st.async + mbarrier (HELR_NTT_XASYNC=0: cluster barriers)
+bool ntt_xasync_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("HELR_NTT_XASYNC");
+        on = e ? (atoi(e) != 0) : 1;
+    }
+    return on != 0;
+}
+
 // external event nodes inside a graph capture, plain records otherwise
 static cudaError_t record(cudaEvent_t ev, cudaStream_t s) {
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;

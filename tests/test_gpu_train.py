@@ -20,7 +20,8 @@ from pathlib import Path
 
 pytestmark = pytest.mark.gpu
 GOLD = Path(__file__).resolve().parent / "golden"
-TOL = 1e-6
+TOL = 1e-6          # BASELINE bar: decrypted weights and AUC within 1e-6
+HEADROOM = TOL / 2  # whole runs must clear the bar with 2x headroom
 
 
 def _run(name, ds, log_n, rows, blocks, mode, n_iters=None, use_graph=True, dnum=2, seed=2):
@@ -67,7 +68,7 @@ def test_medium_whole_run():
     """Medium: all 320 iterations (5 epochs)."""
     w, a = _run("medium", data.medium_dataset(), 15, 1024, 1, "mini_batch")
     print(f"medium 320 it: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
-    assert w < TOL and a < TOL
+    assert w < HEADROOM and a < HEADROOM
 
 
 @pytest.mark.parametrize("seed", [2, 3, 4])
@@ -76,14 +77,14 @@ def test_paper_mini_whole_run(paper_ds, seed):
     key / noise seeds."""
     w, a = _run("paper_mini", paper_ds, 16, 128, 8, "mini_batch", seed=seed)
     print(f"paper_mini 1239 it seed {seed}: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
-    assert w < TOL and a < TOL
+    assert w < HEADROOM and a < HEADROOM
 
 
 def test_paper_full_whole_run(paper_ds):
     """Paper shape, full-batch: all 10 iterations over the 3,304 ciphertexts."""
     w, a = _run("paper_full", paper_ds, 16, 128, 8, "full_batch")
     print(f"paper_full 10 it: max |dw| = {w:.3e}, max |dAUC| = {a:.3e}")
-    assert w < TOL and a < TOL
+    assert w < HEADROOM and a < HEADROOM
 
 
 @pytest.mark.parametrize("mode,blocks", [("mini_batch", 1), ("full_batch", 4)])
