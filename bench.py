@@ -59,7 +59,8 @@ def parse():
     p.add_argument("--no-graph", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-iters", type=int, default=1000, help="bounded CPU-baseline sample (iterations)")
-    p.add_argument("--cpu-rns", action="store_true", help="also time the CPU RNS-CKKS oracle (1 iteration)")
+    p.add_argument("--cpu-rns-iters", type=int, default=1,
+                   help="C3 baseline: iterations of the CPU RNS-CKKS oracle on all host cores (0 = skip)")
     p.add_argument("--profile-steps", type=int, default=4)
     p.add_argument("--dnum", type=int, default=None, help="override the key-switching digit count")
     p.add_argument("--bsgs-bits", type=int, default=None, help="max bits per hoisted group (sum_col_vec)")
@@ -150,10 +151,13 @@ def peaks():
 
 
 def ncu_traffic():
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, if any."""
+    """DRAM bytes per launch of each category from the committed ncu launch
+    list (tools/ncu_summary.py --traffic): an NTT "launch" is one whole
+    transform (both passes), matching the algorithmic bytes per launch."""
     path = ROOT / "profiles" / "ncu_traffic.json"
     try:
-        return json.loads(path.read_text())
+        d = json.loads(path.read_text())
+        return d.get("per_launch", d)
     except Exception:
         return {}
 
@@ -193,6 +197,103 @@ def cpu_reference_sample(wl, iters, warm=0):
     slotsim.train(ds.X, ds.y, wl["log_n"], wl["rows"], wl["blocks"], qpoly, lr_fn, warm + iters, mode=mode,
                   trace=False, stamps=stamps)
     dt = stamps[-1] - stamps[warm]
+    return iters / dt, dt, iters
+
+
+def cpu_rns_sample(wl, iters, cores):
+    """C3: the build's CPU RNS-CKKS oracle (oracle/, plain C +
+    OpenMP on ``cores`` threads) running exactly the arithmetic of one fused
+    iteration of this workload's ring and schedule (oracle/schedule.py) on
+    uniformly random residues and keys (the cost does not depend on values).
+    Returns (iterations/s, timed seconds)."""
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    from oracle import schedule as osched
+    from oracle.oracle import Oracle
+    from paper_2406_13221_b200.driver import grouped_steps
+    from paper_2406_13221_b200.params import CkksParams
+    ck = CkksParams.generate(log_n=wl["log_n"], n_q=wl["L"], dnum=wl["dnum"])
+    orc = Oracle(ck, threads=cores)
+    rng = np.random.default_rng(3)
+    n, L, S = ck.n, ck.L, ck.slots
+    R, C = wl["blocks"], 1
+    log_g = int(math.log2(S // wl["rows"]))
+    log_m = ck.log_n - 1 - log_g
+    lb, lbr = (log_g + 1) // 2, (log_m + 1) // 2
+    q = np.array(ck.q, dtype=np.uint64)[:, None]
+    ct = lambda *lead: (rng.integers(0, 2 ** 62, size=lead + (2, L, n), dtype=np.uint64) % q)
+    beta = -(-L // ck.alpha)
+    pq = np.array(list(ck.q) + list(ck.p), dtype=np.uint64)[:, None]
+    key = lambda: rng.integers(0, 2 ** 62, size=(beta, 2, L + ck.K, n), dtype=np.uint64) % pq
+    steps = [k for grp in grouped_steps(log_g, lb) for k in grp]
+    rsteps = [k for grp in grouped_steps(log_m, lbr, 1 << log_g) for k in grp]
+    gals = set([pow(5, k, 2 * n) for k in steps] + [pow(5, S - k, 2 * n) for k in steps] +
+               [pow(5, k % S, 2 * n) for k in rsteps])
+    gk = {g: key() for g in gals}
+    z, w, v, b = ct(R, C), ct(C), ct(C), ct(C)
+    rlk, mask = key(), ct()[0, 0]
+    consts = rng.integers(0, 2 ** 39, size=(10, L), dtype=np.uint64)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        osched.nag_iteration(orc, z, w, v, b, L - 1, rlk, gk, mask, consts, log_g, log_m, log_baby=lb,
+                             log_baby_rows=lbr)
+    dt = time.perf_counter() - t0
+    return iters / dt, dt
+
+
+def reference_driver_sample(reps=3):
+    """C2: the reference's own driver semantics end to end
+    on Toy — the literal depth-9 ``train_encrypted`` loop (per-iteration
+    decrypt + log-likelihood metrics included) over the reference slot
+    simulator (oracle/slotsim.py behind the SimContext protocol).
+    Returns (iterations/s, seconds, iterations)."""
+    from oracle import slotsim
+    from paper_2406_13221_b200 import enctrain as T
+    from paper_2406_13221_b200.data import toy_dataset
+    from paper_2406_13221_b200.errors import NeedsBootstrap
+    from paper_2406_13221_b200.optimizer import BASELINE_CUBIC, ExpDecay, TrainConfig
+    from paper_2406_13221_b200.params import HeParams
+
+    class Ctx:
+        COUNTER_KEYS = ("enc", "dec", "add", "cadd", "mul", "cmul", "imul", "rotate", "bootstrap")
+
+        def __init__(self, params):
+            self.params = params
+            self._s = slotsim.SlotSim(params.log_n, params.log_q, params.log_delta, params.log_delta_c)
+
+        counters = property(lambda self: self._s.counters, lambda self, v: setattr(self._s, "counters", v))
+
+        def reset_counters(self):
+            snap = dict(self._s.counters)
+            self._s.counters = dict.fromkeys(self.COUNTER_KEYS, 0)
+            return snap
+
+        def __getattr__(self, name):
+            f = getattr(self._s, name)
+
+            def call(*a, **k):
+                try:
+                    return f(*a, **k)
+                except slotsim.SlotNeedsBootstrap as e:
+                    raise NeedsBootstrap(str(e)) from e
+            return call
+
+        def sum_col_vec(self, a, lay):
+            return self.__getattr__("sum_col_vec")(a, lay.m, lay.g)
+
+        def sum_rows(self, a, lay):
+            return self.__getattr__("sum_rows")(a, lay.m, lay.g)
+
+    ds = toy_dataset()
+    params = HeParams(log_n=13, log_q=10 ** 6, log_delta=40, log_delta_c=40)
+    cfg = TrainConfig(mode="mini_batch", batch_size=128, epochs=3, max_iterations=10 ** 6, schedule=ExpDecay(),
+                      sigmoid="g8")
+    t0 = time.perf_counter()
+    iters = runs = 0
+    while runs < reps or time.perf_counter() - t0 < 2.0:   # whole 24-iteration runs, >= 2 s of work
+        res = T.train_encrypted(ds, cfg, params, ctx=Ctx(params), poly=BASELINE_CUBIC)
+        iters += len(res.ledger)
+        runs += 1
+    dt = time.perf_counter() - t0
     return iters / dt, dt, iters
 
 
@@ -313,9 +414,15 @@ def main():
     peak, peak_kind = peaks()
     achieved = (bya[dom] / cna[dom]) / ((msa[dom] / cna[dom]) / 1000.0) / 1e9
     traffic = ncu_traffic().get(CATS[dom])
+    # the event-bracketed replay serialises the graph (no programmatic
+    # dependent-launch overlap), so per-category times add up to more than a
+    # step: shares are reported against the attributed sum
+    attributed = sum(msa) / args.profile_steps
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": CATS[dom], "peak_kind": peak_kind,
-                "share_of_step": (msa[dom] / args.profile_steps) / (ms / steps),
+                "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
+                "kernel": CATS[dom], "peak_kind": peak_kind,
+                "share_of_step": (msa[dom] / args.profile_steps) / attributed,
+                "attributed_ms_per_step": attributed,
                 "algorithmic_bytes_per_launch": bya[dom] / cna[dom],
                 "avg_launch_ms": msa[dom] / cna[dom]}
     step_gb = sum(bya) / args.profile_steps / 1e9
@@ -340,12 +447,24 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ems / steps}
         tr.disable_host_stream()
 
-    # ---------------- CPU baseline (rank 0, N=1 only)
+    # ---------------- CPU baselines (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and args.cpu_iters > 0:
+        nproc = os.cpu_count() or 1
         rate, dt, iters = cpu_reference_sample(wl, args.cpu_iters, warm=5)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{iters} iterations of the reference simulator circuit (oracle/slotsim.py), {dt:.1f} s"}
+               "sample": f"C1: {iters} iterations of the reference simulator circuit (oracle/slotsim.py, numpy "
+                         f"elementwise: one core of {nproc}), {dt:.1f} s"}
+        r2, dt2, it2 = reference_driver_sample()
+        cpu["reference_driver"] = {"value": r2, "unit": UNIT, "cores": 1, "kind": "port", "workload": "toy",
+                                   "sample": f"C2: {it2} iterations of the literal train_encrypted loop with its "
+                                             f"per-iteration metrics over the reference simulator, Toy, {dt2:.1f} s"}
+        if args.cpu_rns_iters > 0:
+            r3, dt3 = cpu_rns_sample(wl, args.cpu_rns_iters, nproc)
+            cpu["rns_oracle"] = {"value": r3, "unit": UNIT, "cores": nproc, "kind": "port",
+                                 "sample": f"C3: {args.cpu_rns_iters} fused iteration(s) of the CPU RNS-CKKS oracle "
+                                           f"(real HE, same ring and schedule as the GPU), {dt3:.1f} s on {nproc} "
+                                           f"OpenMP threads", "gpu_speedup": value / r3}
 
     if rank == 0:
         line = {

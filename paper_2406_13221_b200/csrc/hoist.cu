@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "async.cuh"
 #include "ks.cuh"
 
 // Per-thread asynchronous prefetch: every thread copies the key words and

@@ -12,140 +12,6 @@
 
 #include "ks.cuh"
 
-// ---------------------------------------------------------------------------
-// key switching
-struct KsInput {
-    const u64* d;        // NTT-form polynomial of item b at d + b*d_stride, limb stride N
-    long long d_stride;
-    long long galois;    // 0: none, else apply X -> X^galois to d first
-};
-struct KsEpilogue {
-    u64* out;             // ciphertext of item b at out + b*out_stride
-    long long out_stride;
-    const u64* add_a;     // optional ciphertext-like addend (both polys), stride add_a_stride
-    long long add_a_stride;
-    const u64* add_p;     // optional: sum_t sigma_t(poly 0 of add_p) added to out poly 0
-    long long add_p_stride;
-    int ngal;
-    long long gal[HELR_MAX_HOIST];
-};
-static KsEpilogue make_epilogue(u64* out, long long os, const u64* add_a, long long as, const u64* add_p, long long ps,
-                                int ngal, const long long* gal) {
-    KsEpilogue e;
-    e.out = out; e.out_stride = os; e.add_a = add_a; e.add_a_stride = as; e.add_p = add_p; e.add_p_stride = ps;
-    e.ngal = ngal;
-    for (int t = 0; t < HELR_MAX_HOIST; t++) e.gal[t] = t < ngal ? gal[t] : 0;
-    return e;
-}
-
-// ModUp conversion for digit j; grid (x: coeff tiles, y: digit, z: item)
-struct ModUpArgs {
-    const u64* coef;   // [B][nl][N] INTT of d
-    long long coef_stride;
-    const u64* d;      // NTT-form input (own-digit limbs are copied from here)
-    long long d_stride;
-    long long galois;
-    u64* ext;          // [B][beta][ext][N]
-    long long ext_item_stride, ext_digit_stride;
-    const u64* tab;    // d_tab
-    const size_t* offs;// device array of modup offsets for this level (per digit)
-    int n, log_n, nl, K, L, alpha;
-};
-// Two consecutive coefficients per thread, 16-byte accesses; register
-// arrays bounded by the template parameter (alpha / K <= MA).
-
-template <int MA>
-__global__ void k_modup(ModUpArgs a, Tables tb) {
-    pdl_begin();
-    const int j = blockIdx.y, b = blockIdx.z;
-    const int lo = j * a.alpha, hi = lo + a.alpha < a.nl ? lo + a.alpha : a.nl;
-    const int ns = hi - lo;
-    const int ne = a.nl + a.K;
-    const int nt = ne - ns;
-    const u64* T = a.tab + a.offs[j];
-    const u64* hv = T;
-    const u64* hvs = T + ns;
-    const u64* hm = T + 2 * ns;
-    const u64* hms = hm + (size_t)ns * nt;
-    u64* ext = a.ext + (size_t)b * a.ext_item_stride + (size_t)j * a.ext_digit_stride;
-    const u64* coef = a.coef + (size_t)b * a.coef_stride;
-    const u64* d = a.d + (size_t)b * a.d_stride;
-    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i >= a.n) return;
-    u64 y0[MA], y1[MA];
-#pragma unroll
-    for (int k = 0; k < MA; k++) {
-        if (k < ns) {
-            const int p = lo + k;
-            const ulonglong2 c = ld2(coef + (size_t)p * a.n + i);
-            y0[k] = shoup(c.x, hv[k], hvs[k], tb.q[p]);
-            y1[k] = shoup(c.y, hv[k], hvs[k], tb.q[p]);
-            // own-digit limbs: the NTT-form input itself (exact doubles for fp64 limbs)
-            ulonglong2 v;
-            if (a.galois) {
-                const u64* dp = d + (size_t)p * a.n;
-                v = make_ulonglong2(dp[galois_perm(i, (u64)a.galois, a.log_n)],
-                                    dp[galois_perm(i + 1, (u64)a.galois, a.log_n)]);
-            } else {
-                v = ld2(d + (size_t)p * a.n + i);
-            }
-            if (tb.q[p] < NTT_DBL_BOUND)
-                v = make_ulonglong2((u64)__double_as_longlong(u2d(v.x)), (u64)__double_as_longlong(u2d(v.y)));
-            *reinterpret_cast<ulonglong2*>(ext + (size_t)p * a.n + i) = v;
-        }
-    }
-    // source residues as exact doubles (primes < 2^41) for the fp64 targets
-    double yd0[MA], yd1[MA];
-    bool ydok[MA];
-#pragma unroll
-    for (int k = 0; k < MA; k++) {
-        ydok[k] = k < ns && tb.q[lo + k] < NTT_DBL_BOUND;
-        if (ydok[k]) { yd0[k] = u2d(y0[k]); yd1[k] = u2d(y1[k]); }
-    }
-    int t = 0;
-    for (int e = 0; e < ne; e++) {
-        if (e >= lo && e < hi) continue;
-        const int p = e < a.nl ? e : a.L + (e - a.nl);
-        const u64 q = tb.q[p];
-        if (q < NTT_DBL_BOUND) {
-            // fp64 target: exact signed products (mulmod_d), one reduction
-            const DblC dc{tb.qd[p], tb.qinvd[p]};
-            double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-            for (int k = 0; k < MA; k++) {
-                if (k < ns) {
-                    const u64 w = hm[(size_t)k * nt + t];
-                    if (ydok[k]) {
-                        const double wd = u2d(w);
-                        s0 = __dadd_rn(s0, mulmod_d(yd0[k], wd, dc));
-                        s1 = __dadd_rn(s1, mulmod_d(yd1[k], wd, dc));
-                    } else {  // wide source prime (q_0): integer Shoup, result < q
-                        const u64 ws = hms[(size_t)k * nt + t];
-                        s0 = __dadd_rn(s0, u2d(shoup(y0[k], w, ws, q)));
-                        s1 = __dadd_rn(s1, u2d(shoup(y1[k], w, ws, q)));
-                    }
-                }
-            }
-            // raw signed double (|x| <= q/2 + 1): the NTT below reads it as is (in_raw)
-            st2(ext + (size_t)e * a.n + i, (u64)__double_as_longlong(reduce_d(s0, dc)),
-                (u64)__double_as_longlong(reduce_d(s1, dc)));
-            t++;
-            continue;
-        }
-        u64 s0 = 0, s1 = 0;
-#pragma unroll
-        for (int k = 0; k < MA; k++) {
-            if (k < ns) {
-                const u64 w = hm[(size_t)k * nt + t], ws = hms[(size_t)k * nt + t];
-                s0 = add_mod(s0, shoup(y0[k], w, ws, q), q);
-                s1 = add_mod(s1, shoup(y1[k], w, ws, q), q);
-            }
-        }
-        st2(ext + (size_t)e * a.n + i, s0, s1);
-        t++;
-    }
-}
-
 // inner product: acc[b][poly][e] = sum_j ext[b][j][e] * evk[j][poly][prime(e)]
 // block (64, <= 8): threadIdx.y = ciphertext, so the 8 warps of a block read
 // the same key words (one DRAM read, L1 hits for the rest).
@@ -239,219 +105,6 @@ __global__ void k_ks_inner(const u64* ext, long long ext_item_stride, long long 
     st2(ap + ((size_t)(nl + K) + e) * n + i, o10, o11);
 }
 
-// ModDown conversion: mdc[b][poly][i] = sum_k [a_k * phinv_k]_{p_k} * phmod[k][i] mod q_i
-// Centred conversion (see oracle oc_moddown_convert): subtract r*P with
-// r = round(sum_k y_k / p_k) evaluated in IEEE double without contraction,
-// so the ModDown error is the zero-mean rounding of x / P.
-template <int MK>
-__global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n,
-                               int nl, int K, int L, const u64* phinv, const u64* phinv_sh, const u64* phm,
-                               const u64* phms, const u64* pinv_dbl, const u64* pm, const u64* pm_sh, Tables tb) {
-    pdl_begin();
-    const int it = blockIdx.y;  // item*2 + poly
-    const int b = it >> 1, poly = it & 1;
-    const int ne = nl + K;
-    const u64* ap = acc + (size_t)b * acc_item_stride + (size_t)poly * ne * n;
-    u64* mp = mdc + (size_t)b * mdc_item_stride + (size_t)poly * L * n;
-    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i >= n) return;
-    u64 z0[MK], z1[MK];
-    double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < MK; k++) {
-        if (k < K) {
-            const u64 pk = tb.q[L + k];
-            const double inv = __longlong_as_double((long long)pinv_dbl[k]);
-            const ulonglong2 x = ld2(ap + (size_t)(nl + k) * n + i);
-            double d0, d1;  // canonical z as exact doubles (no u64 -> f64 conversions)
-            if (pk < NTT_DBL_BOUND) {
-                const DblC dk{tb.qd[L + k], tb.qinvd[L + k]};
-                const double w = u2d(phinv[k]);
-                d0 = d2d_canon(mulmod_d(u2d(x.x), w, dk), dk);
-                d1 = d2d_canon(mulmod_d(u2d(x.y), w, dk), dk);
-                z0[k] = dexact(d0);
-                z1[k] = dexact(d1);
-            } else {
-                z0[k] = shoup(x.x, phinv[k], phinv_sh[k], pk);
-                z1[k] = shoup(x.y, phinv[k], phinv_sh[k], pk);
-                d0 = __ull2double_rn(z0[k]);
-                d1 = __ull2double_rn(z1[k]);
-            }
-            v0 = __dadd_rn(v0, __dmul_rn(d0, inv));
-            v1 = __dadd_rn(v1, __dmul_rn(d1, inv));
-        }
-    }
-    const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
-    const u64 rr1 = (u64)__double2ull_rd(__dadd_rn(v1, 0.5));
-    // sources as exact doubles when every special prime is below 2^41
-    bool dsrc = true;
-    double zd0[MK], zd1[MK];
-#pragma unroll
-    for (int k = 0; k < MK; k++) {
-        if (k < K) {
-            dsrc = dsrc && tb.q[L + k] < NTT_DBL_BOUND;
-            zd0[k] = u2d(z0[k] & 0x000FFFFFFFFFFFFFull);
-            zd1[k] = u2d(z1[k] & 0x000FFFFFFFFFFFFFull);
-        }
-    }
-    for (int p = 0; p < nl; p++) {
-        const u64 q = tb.q[p];
-        if (dsrc && q < NTT_DBL_BOUND) {  // fp64 target (see k_modup)
-            const DblC dc{tb.qd[p], tb.qinvd[p]};
-            const double pmd = u2d(pm[p]);
-            double s0 = -__dmul_rn(u2d(rr0), pmd), s1 = -__dmul_rn(u2d(rr1), pmd);  // exact: rr < K + 1
-#pragma unroll
-            for (int k = 0; k < MK; k++) {
-                if (k < K) {
-                    const double wd = u2d(phm[(size_t)k * L + p]);
-                    s0 = __dadd_rn(s0, mulmod_d(zd0[k], wd, dc));
-                    s1 = __dadd_rn(s1, mulmod_d(zd1[k], wd, dc));
-                }
-            }
-            // raw signed doubles: the NTT that follows reads them as is (in_raw)
-            st2(mp + (size_t)p * n + i, (u64)__double_as_longlong(reduce_d(s0, dc)),
-                (u64)__double_as_longlong(reduce_d(s1, dc)));
-            continue;
-        }
-        u64 s0 = 0, s1 = 0;
-#pragma unroll
-        for (int k = 0; k < MK; k++) {
-            if (k < K) {
-                const u64 w = phm[(size_t)k * L + p], ws = phms[(size_t)k * L + p];
-                s0 = add_mod(s0, shoup(z0[k], w, ws, q), q);
-                s1 = add_mod(s1, shoup(z1[k], w, ws, q), q);
-            }
-        }
-        st2(mp + (size_t)p * n + i, sub_mod(s0, shoup(rr0, pm[p], pm_sh[p], q), q),
-            sub_mod(s1, shoup(rr1, pm[p], pm_sh[p], q), q));
-    }
-}
-
-
-// Loader applying the Galois permutation to a plain buffer (rotation input).
-struct LdPerm {
-    const u64* base;
-    long long item_stride;
-    int n, log_n;
-    u64 g;
-    __device__ __forceinline__ u64 operator()(int z, int li, int, int off) const {
-        return base[(size_t)z * item_stride + (size_t)li * n + galois_perm(off, g, log_n)];
-    }
-};
-
-// ModUp of B inputs into w.ext (NTT form over Q_l + P for every digit)
-static int ks_modup(helr_ctx* c, KsInput in, int level, int B, const KsWs& w, cudaStream_t s) {
-    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
-    const int nd = (nl + c->alpha - 1) / c->alpha;
-    // 1) coef = INTT(sigma(d))
-    {
-        LimbMap m = limb_range(0, nl);
-        StBuf st{w.coef, w.coef_s, m, n};
-        if (in.galois) {
-            LdPerm ld{in.d, in.d_stride, n, c->log_n, (u64)in.galois};
-            ntt_launch<true>(c, ld, st, w.coef, w.coef_s, m, B, s);
-        } else {
-            LdBuf ld{in.d, in.d_stride, m, n};
-            ntt_launch<true>(c, ld, st, w.coef, w.coef_s, m, B, s);
-        }
-        CHECK_LAUNCH("ks intt");
-    }
-    // 2) ModUp conversions (+ copy of own-digit NTT limbs)
-    {
-        ModUpArgs a{w.coef, w.coef_s, in.d, in.d_stride, in.galois, w.ext, w.ext_s, w.ext_ds, c->d_tab,
-                    c->d_modup_offs + (size_t)level * c->beta, n, c->log_n, nl, K, L, c->alpha};
-        dim3 g(blocks_for(n / 2, 128), nd, B);
-        ProfScope ps(PROF_MODUP, 8.0 * n * B * (2.0 * nl + (double)nd * ne), s);
-        if (c->alpha <= 4) launch_pdl(k_modup<4>, g, dim3(128), 0, s, a, c->t);
-        else if (c->alpha <= 8) launch_pdl(k_modup<8>, g, dim3(128), 0, s, a, c->t);
-        else if (c->alpha <= 16) launch_pdl(k_modup<16>, g, dim3(128), 0, s, a, c->t);
-        else if (c->alpha <= 32) launch_pdl(k_modup<32>, g, dim3(128), 0, s, a, c->t);
-        else launch_pdl(k_modup<HELR_MAXP>, g, dim3(128), 0, s, a, c->t);
-        CHECK_KERNEL("ks modup");
-    }
-    // 3) NTT of every converted limb of every digit (one launch per 128 limbs)
-    {
-        LimbMap m;
-        m.count = 0;
-        for (int j = 0; j < nd; j++) {
-            const int lo = j * c->alpha, hi = lo + c->alpha < nl ? lo + c->alpha : nl;
-            for (int e = 0; e < ne; e++) {
-                if (e >= lo && e < hi) continue;
-                m.off[m.count] = (unsigned char)(j * c->LK + e);
-                m.prime[m.count] = (unsigned char)(e < nl ? e : L + (e - nl));
-                if (++m.count == HELR_MAXLIMBS) {
-                    ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, m, B, s, 1, 1);
-                    m.count = 0;
-                }
-            }
-        }
-        // fp64 limbs: raw doubles in, exact (canonical) doubles out — the inner
-        // products split them on the fp64 pipe (split21_d).  Integer-path
-        // limbs (q_0) first: the limb is the grid's slowest index, so the
-        // slower CTAs start in the first waves.
-        if (m.count) {
-            LimbMap h;
-            h.count = 0;
-            for (int pass = 0; pass < 2; pass++)
-                for (int i = 0; i < m.count; i++)
-                    if ((c->primes[m.prime[i]] >= NTT_DBL_BOUND) == (pass == 0)) {
-                        h.off[h.count] = m.off[i];
-                        h.prime[h.count++] = m.prime[i];
-                    }
-            ntt_buffers<false>(c, w.ext, w.ext_s, w.ext, w.ext_s, h, B, s, 1, 1);
-        }
-        CHECK_LAUNCH("ks modup ntt");
-    }
-    return HELR_OK;
-}
-
-// ModDown of w.acc (both polynomials) and the fused epilogue into ep.out
-static int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const KsWs& w, cudaStream_t s) {
-    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K;
-    LimbMap m;
-    m.count = 2 * K;  // P limbs of both polynomials in one launch
-    for (int poly = 0; poly < 2; poly++)
-        for (int k = 0; k < K; k++) {
-            m.off[poly * K + k] = (unsigned char)(poly * ne + nl + k);
-            m.prime[poly * K + k] = (unsigned char)(L + k);
-        }
-    ntt_buffers<true>(c, w.acc, w.acc_s, w.acc, w.acc_s, m, B, s);
-    CHECK_LAUNCH("ks moddown intt");
-    dim3 g(blocks_for(n / 2, 128), 2 * B);
-    {
-        ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + nl), s);
-        // register arrays sized to K (dnum 1 rings have K up to ~31)
-        auto conv = K <= 4 ? k_moddown_conv<4>
-                  : K <= 8 ? k_moddown_conv<8>
-                  : K <= 16 ? k_moddown_conv<16>
-                  : K <= 32 ? k_moddown_conv<32> : k_moddown_conv<HELR_MAXP>;
-        launch_pdl(conv, g, dim3(128), 0, s, (const u64*)w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv,
-                   c->md_phinv_sh, c->md_phmod, c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
-        CHECK_KERNEL("ks moddown conv");
-    }
-    LimbMap mq;
-    mq.count = 2 * nl;
-    for (int poly = 0; poly < 2; poly++)
-        for (int i = 0; i < nl; i++) {
-            mq.off[poly * nl + i] = (unsigned char)(poly * L + i);
-            mq.prime[poly * nl + i] = (unsigned char)i;
-        }
-    // NTT of the conversion; its last pass applies (acc - conv) * P^-1 and
-    // the epilogue addends while storing (StCombine)
-    {
-        LdBuf ld{w.mdc, w.mdc_s, mq, n};
-        StCombine st = st_combine(c, ep.out, ep.out_stride, (long long)L * n, w.acc, w.acc_s, (long long)ne * n,
-                                  c->md_pinv, c->md_pinv_sh, nl);
-        st.add_a = ep.add_a; st.a_is = ep.add_a_stride; st.a_ps = (long long)L * n;
-        st.add_p = ep.add_p; st.p_is = ep.add_p_stride;
-        st.ngal = ep.add_p ? ep.ngal : 0;
-        for (int t = 0; t < HELR_MAX_HOIST; t++) st.gal[t] = ep.gal[t];
-        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s, 1);
-        CHECK_LAUNCH("ks moddown ntt+final");
-    }
-    return HELR_OK;
-}
-
 // single-key inner product (relinearisation / one rotation): with one key
 // there is no step loop to prefetch across, so the 2-coefficient, ciphertext-
 // row kernel (k_ks_inner) is faster than the hoisted kernel here
@@ -476,146 +129,6 @@ static int keyswitch_batch(helr_ctx* c, KsInput in, const u64* evk, int level, c
     r = key_inner_single(c, w, evk, B, level, nullptr, 0, s);
     if (r) return r;
     return ks_moddown(c, level, ep, B, w, s);
-}
-
-// ---- merged ModDown + rescale --------------------------------------------
-// acc (PQ_l basis, Q limbs already holding acc + P d) -> round(acc / (P q_l))
-// over Q_{l-1}: centred fast conversion from {p_0..p_{K-1}, q_l} (coefficient
-// form) to Q_{l-1}, NTT, then (acc_i - conv_i) * (P q_l)^-1.  Saves the
-// separate rescale's INTT + l NTTs per polynomial.
-struct MrTab {
-    const u64 *hv, *hvs, *hm, *hms, *mm, *mms, *mi, *mis, *dinv;
-};
-static MrTab mr_tab(const helr_ctx* c, int level) {
-    const int ns = c->K + 1, L = c->L;
-    const u64* e = c->d_tab + c->mr_off[level];
-    MrTab t;
-    t.hv = e; t.hvs = e + ns; t.hm = t.hvs + ns; t.hms = t.hm + (size_t)ns * L; t.mm = t.hms + (size_t)ns * L;
-    t.mms = t.mm + L; t.mi = t.mms + L; t.mis = t.mi + L; t.dinv = t.mis + L;
-    return t;
-}
-template <int MK>
-__global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n, int nl,
-                           int K, int L, MrTab mt, Tables tb) {
-    pdl_begin();
-    const int it = blockIdx.y;  // item*2 + poly
-    const int b = it >> 1, poly = it & 1;
-    const int ne = nl + K, l = nl - 1, ns = K + 1;
-    const u64* ap = acc + (size_t)b * acc_item_stride + (size_t)poly * ne * n;
-    u64* mp = mdc + (size_t)b * mdc_item_stride + (size_t)poly * L * n;
-    const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i >= n) return;
-    u64 z0[MK], z1[MK];
-    double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < MK; k++) {
-        if (k < ns) {
-            const int lim = k < K ? nl + k : l;
-            const u64 m = tb.q[k < K ? L + k : l];
-            const double inv = __longlong_as_double((long long)mt.dinv[k]);
-            const ulonglong2 x = ld2(ap + (size_t)lim * n + i);
-            double d0, d1;  // canonical z as exact doubles (no u64 -> f64 conversions)
-            if (m < NTT_DBL_BOUND) {
-                const int pm = k < K ? L + k : l;
-                const DblC dk{tb.qd[pm], tb.qinvd[pm]};
-                const double w = u2d(mt.hv[k]);
-                d0 = d2d_canon(mulmod_d(u2d(x.x), w, dk), dk);
-                d1 = d2d_canon(mulmod_d(u2d(x.y), w, dk), dk);
-                z0[k] = dexact(d0);
-                z1[k] = dexact(d1);
-            } else {
-                z0[k] = shoup(x.x, mt.hv[k], mt.hvs[k], m);
-                z1[k] = shoup(x.y, mt.hv[k], mt.hvs[k], m);
-                d0 = __ull2double_rn(z0[k]);
-                d1 = __ull2double_rn(z1[k]);
-            }
-            v0 = __dadd_rn(v0, __dmul_rn(d0, inv));
-            v1 = __dadd_rn(v1, __dmul_rn(d1, inv));
-        }
-    }
-    const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
-    const u64 rr1 = (u64)__double2ull_rd(__dadd_rn(v1, 0.5));
-    bool dsrc = true;
-    double zd0[MK], zd1[MK];
-#pragma unroll
-    for (int k = 0; k < MK; k++) {
-        if (k < ns) {
-            dsrc = dsrc && tb.q[k < K ? L + k : l] < NTT_DBL_BOUND;
-            zd0[k] = u2d(z0[k] & 0x000FFFFFFFFFFFFFull);
-            zd1[k] = u2d(z1[k] & 0x000FFFFFFFFFFFFFull);
-        }
-    }
-    for (int p = 0; p < l; p++) {
-        const u64 q = tb.q[p];
-        if (dsrc && q < NTT_DBL_BOUND) {  // fp64 target (see k_modup)
-            const DblC dc{tb.qd[p], tb.qinvd[p]};
-            const double mmd = u2d(mt.mm[p]);
-            double s0 = -__dmul_rn(u2d(rr0), mmd), s1 = -__dmul_rn(u2d(rr1), mmd);  // exact: rr <= K + 1
-#pragma unroll
-            for (int k = 0; k < MK; k++) {
-                if (k < ns) {
-                    const double wd = u2d(mt.hm[(size_t)k * L + p]);
-                    s0 = __dadd_rn(s0, mulmod_d(zd0[k], wd, dc));
-                    s1 = __dadd_rn(s1, mulmod_d(zd1[k], wd, dc));
-                }
-            }
-            st2(mp + (size_t)p * n + i, (u64)__double_as_longlong(reduce_d(s0, dc)),
-                (u64)__double_as_longlong(reduce_d(s1, dc)));  // raw (in_raw NTT)
-            continue;
-        }
-        u64 s0 = 0, s1 = 0;
-#pragma unroll
-        for (int k = 0; k < MK; k++) {
-            if (k < ns) {
-                const u64 w = mt.hm[(size_t)k * L + p], ws = mt.hms[(size_t)k * L + p];
-                s0 = add_mod(s0, shoup(z0[k], w, ws, q), q);
-                s1 = add_mod(s1, shoup(z1[k], w, ws, q), q);
-            }
-        }
-        st2(mp + (size_t)p * n + i, sub_mod(s0, shoup(rr0, mt.mm[p], mt.mms[p], q), q),
-            sub_mod(s1, shoup(rr1, mt.mm[p], mt.mms[p], q), q));
-    }
-}
-
-static int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, int B, const KsWs& w, cudaStream_t s) {
-    const int n = c->n, nl = level + 1, K = c->K, L = c->L, ne = nl + K, l = level;
-    MrTab mt = mr_tab(c, level);
-    LimbMap m;
-    m.count = 2 * (K + 1);
-    for (int poly = 0; poly < 2; poly++) {
-        for (int k = 0; k < K; k++) {
-            m.off[poly * (K + 1) + k] = (unsigned char)(poly * ne + nl + k);
-            m.prime[poly * (K + 1) + k] = (unsigned char)(L + k);
-        }
-        m.off[poly * (K + 1) + K] = (unsigned char)(poly * ne + l);
-        m.prime[poly * (K + 1) + K] = (unsigned char)l;
-    }
-    ntt_buffers<true>(c, w.acc, w.acc_s, w.acc, w.acc_s, m, B, s);
-    CHECK_LAUNCH("mdr intt");
-    {
-        dim3 g(blocks_for(n / 2, 128), 2 * B);
-        ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + 1 + l), s);
-        auto conv = K + 1 <= 4 ? k_mdr_conv<4>
-                  : K + 1 <= 8 ? k_mdr_conv<8>
-                  : K + 1 <= 16 ? k_mdr_conv<16>
-                  : K + 1 <= 32 ? k_mdr_conv<32> : k_mdr_conv<HELR_MAXP>;
-        launch_pdl(conv, g, dim3(128), 0, s, (const u64*)w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, mt, c->t);
-        CHECK_KERNEL("mdr conv");
-    }
-    LimbMap mq;
-    mq.count = 2 * l;
-    for (int poly = 0; poly < 2; poly++)
-        for (int i = 0; i < l; i++) {
-            mq.off[poly * l + i] = (unsigned char)(poly * L + i);
-            mq.prime[poly * l + i] = (unsigned char)i;
-        }
-    {
-        LdBuf ld{w.mdc, w.mdc_s, mq, n};
-        const StCombine st = st_combine(c, out, os, (long long)L * n, w.acc, w.acc_s, (long long)ne * n, mt.mi, mt.mis, l);
-        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s, 1);
-        CHECK_LAUNCH("mdr ntt+final");
-    }
-    return HELR_OK;
 }
 
 // ---- hoisted rotate-and-sum ------------------------------------------------

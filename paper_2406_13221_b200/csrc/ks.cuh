@@ -252,3 +252,32 @@ struct HoistKeys {
 // (P mod q) * (d0, d1) of a [B][3][L][N] tensor to the Q limbs
 int key_inner(helr_ctx* c, const KsWs& w, const HoistKeys& hk, int nb, int level, const u64* dadd, long long dadd_is,
               cudaStream_t s);
+
+// ---- key-switching stages shared by ks.cu / ks_modup.cu / ks_moddown.cu
+struct KsInput {
+    const u64* d;        // NTT-form polynomial of item b at d + b*d_stride, limb stride N
+    long long d_stride;
+    long long galois;    // 0: none, else apply X -> X^galois to d first
+};
+struct KsEpilogue {
+    u64* out;             // ciphertext of item b at out + b*out_stride
+    long long out_stride;
+    const u64* add_a;     // optional ciphertext-like addend (both polys), stride add_a_stride
+    long long add_a_stride;
+    const u64* add_p;     // optional: sum_t sigma_t(poly 0 of add_p) added to out poly 0
+    long long add_p_stride;
+    int ngal;
+    long long gal[HELR_MAX_HOIST];
+};
+static inline KsEpilogue make_epilogue(u64* out, long long os, const u64* add_a, long long as, const u64* add_p, long long ps,
+                                int ngal, const long long* gal) {
+    KsEpilogue e;
+    e.out = out; e.out_stride = os; e.add_a = add_a; e.add_a_stride = as; e.add_p = add_p; e.add_p_stride = ps;
+    e.ngal = ngal;
+    for (int t = 0; t < HELR_MAX_HOIST; t++) e.gal[t] = t < ngal ? gal[t] : 0;
+    return e;
+}
+
+int ks_modup(helr_ctx* c, KsInput in, int level, int B, const KsWs& w, cudaStream_t s);
+int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const KsWs& w, cudaStream_t s);
+int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, int B, const KsWs& w, cudaStream_t s);

@@ -690,7 +690,15 @@ inline int ntt_split_s1(int log_n) { return log_n / 2; }
 template <class St>
 inline double ntt_extra_words(const St&, const LimbMap&, int) { return 0.0; }
 
+// single-pass 8-CTA cluster NTT for N = 2^16 (ntt_cluster.cuh): measured
+// slower than the two passes below, so it is only compiled
+// with -DHELR_NTT_CLUSTER_BUILD=1 (HELR_NVCC_DEFS) and enabled by HELR_NTT_CLUSTER=1
+#ifndef HELR_NTT_CLUSTER_BUILD
+#define HELR_NTT_CLUSTER_BUILD 0
+#endif
+#if HELR_NTT_CLUSTER_BUILD
 #include "ntt_cluster.cuh"
+#endif
 
 
 template <bool INV, class Ld, class St>
@@ -702,10 +710,12 @@ static void ntt_launch(const helr_ctx* c, const Ld& ld, const St& st, u64* mid, 
     // algorithmic bytes: every limb read and written once, plus the extra
     // operands a fused storer reads once (StCombine: ntt_extra_words)
     ProfScope ps(PROF_NTT, 8.0 * c->n * (2.0 * map.count * count + ntt_extra_words(st, map, count)), s);
+#if HELR_NTT_CLUSTER_BUILD
     if (log_n == ncl::LOG_N && ntt_cluster_enabled((long long)map.count * count)) {
         ntt_cluster_launch<INV>(ld, st, c->t, map, count, s, in_raw, out_dbl);
         return;
     }
+#endif
     if (log_n <= 11) {
         ntt_single<INV>(log_n, ld, st, c->t, map, count, s, in_raw, out_dbl);
         return;

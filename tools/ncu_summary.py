@@ -120,9 +120,19 @@ def main():
         with open(a.md, "w") as fh:
             fh.write(text)
     if a.traffic:
-        tr = {c: s["dram"] / s["launches"] for c, s in cats.items() if s["launches"] and s["has_dram"]}
-        tr["_source"] = a.csv
-        tr["_unit"] = "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu serialised)"
+        per_kernel = {c: s["dram"] / s["launches"] for c, s in cats.items() if s["launches"] and s["has_dram"]}
+        # an NTT "launch" in the library's byte model (ProfScope in ntt_launch)
+        # is one whole transform: two ntt_pass kernels (N >= 2^12) or one
+        # ntt_cluster kernel, so DRAM bytes are summed over both passes
+        n_pass = sum(1 for d in launches if "ntt_pass" in d["name"])
+        n_cl = sum(1 for d in launches if "ntt_cluster" in d["name"])
+        per_launch = dict(per_kernel)
+        if cats["ntt"]["has_dram"] and (n_pass or n_cl):
+            per_launch["ntt"] = cats["ntt"]["dram"] / (n_pass / 2.0 + n_cl)
+        tr = {"per_launch": per_launch, "per_kernel_launch": per_kernel,
+              "ntt_transforms": n_pass / 2.0 + n_cl, "_source": a.csv,
+              "_unit": "DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum, ncu serialised, cold cache); "
+                       "per_launch: per library launch (NTT: per two-pass transform), per_kernel_launch: per CUDA kernel"}
         with open(a.traffic, "w") as fh:
             json.dump(tr, fh, indent=1)
 
