@@ -137,6 +137,12 @@ int helr_reduce(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count, int 
 /* Drop q_level: out (level-1) = round(in / q_level). */
 int helr_rescale(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count,
                  int level, void* stream);
+/* ModRaise, the first step of real CKKS bootstrapping (the reference only
+ * models a bootstrap: SimContext.bootstrap, hesim.py:228-236): read `a`
+ * modulo q_0 (any level; only limb 0 is used) and re-interpret the centred
+ * coefficients modulo q_0..q_level_out.  out encrypts m + q_0 * I. */
+int helr_mod_raise(helr_ctx* ctx, const uint64_t* a, uint64_t* out, int count,
+                   int level_out, void* stream);
 /* ct x ct product with relinearisation (no rescale): out = relin(a*b). */
 int helr_mul_relin(helr_ctx* ctx, const uint64_t* a, const uint64_t* b,
                    const uint64_t* rlk, uint64_t* out, int count, int level,

@@ -822,6 +822,31 @@ void oc_rotate(oc_ctx* c, const u64* a, int64_t galois, const u64* gk, u64* out,
         free(r0); free(r1); free(k0); free(k1);
     }
 }
+/* ModRaise (bootstrapping step 1): coefficients of a modulo q_0, centred to
+ * (-q_0/2, q_0/2], re-read modulo q_0..q_level_out.  Textbook definition
+ * (Cheon-Han-Kim-Kim-Song 2018, section 4.1); the reference only models the
+ * bootstrap's level reset (hesim.py:228-236). */
+void oc_mod_raise(oc_ctx* c, const u64* a, u64* out, int count, int level_out) {
+    int N = c->n;
+    u64 q0 = c->prm[0], half = q0 >> 1;
+    for (int x = 0; x < count; x++)
+        for (int k = 0; k < 2; k++) {
+            u64* r = (u64*)malloc(sizeof(u64) * N);
+            memcpy(r, CT(a, x, k, 0), sizeof(u64) * N);
+            oc_intt(c, r, 0);
+            for (int p = 0; p <= level_out; p++) {
+                u64 q = c->prm[p];
+                u64* o = CT(out, x, k, p);
+                for (int i = 0; i < N; i++) {
+                    u64 v = r[i];
+                    if (v > half) { u64 m = (q0 - v) % q; o[i] = m ? q - m : 0; }
+                    else o[i] = v % q;
+                }
+                oc_ntt(c, o, p);
+            }
+            free(r);
+        }
+}
 void oc_refresh(oc_ctx* c, const u64* sk, const u64* a, int in_level, double ratio, u64* out, int out_level,
                 int count, u64 seed, u64 first_id) {
     (void)in_level;

@@ -75,6 +75,7 @@ def lib():
             "oc_mul_relin": (None, [vp, _u64p, _u64p, _u64p, _u64p, ctypes.c_int, ctypes.c_int]),
             "oc_automorph": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
             "oc_rotate": (None, [vp, _u64p, ctypes.c_int64, _u64p, _u64p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+            "oc_mod_raise": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_int]),
             "oc_refresh": (None, [vp, _u64p, _u64p, ctypes.c_int, ctypes.c_double, _u64p, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64]),
         }
@@ -277,6 +278,12 @@ class Oracle:
         ks = [np.ascontiguousarray(k) for k in keys]
         arr = (_u64p * len(ks))(*[_p(k) for k in ks])
         lib().oc_rotsum(self._h, _p(a), len(ks), _p(g), arr, _p(out), a.shape[0], level, 1 if include_identity else 0)
+        return out
+
+    def mod_raise(self, a, level_out):
+        a = np.ascontiguousarray(a)
+        out = self._out(a)
+        lib().oc_mod_raise(self._h, _p(a), _p(out), a.shape[0], level_out)
         return out
 
     def refresh(self, sk, a, in_level, ratio, out_level, seed, first_id):

@@ -54,6 +54,7 @@ SIGNATURES = {
     "helr_metrics": [_vp, _vp, _vp, _vp, _i, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp],
     "helr_metrics_scratch": None,  # returns size_t (bound in metrics.py)
     "helr_rescale": [_vp, _u64p, _u64p, _i, _i, _vp],
+    "helr_mod_raise": [_vp, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_relin": [_vp, _u64p, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_mul_relin_rescale": [_vp, _u64p, _u64p, _u64p, _u64p, _i, _i, _vp],
     "helr_imul": [_vp, _u64p, _u64p, _i, _i, _vp],

@@ -475,6 +475,60 @@ extern "C" int helr_rescale(helr_ctx* c, const uint64_t* a, uint64_t* out, int c
     return op_rescale(c, (const u64*)a, cs, (u64*)out, cs, count, level, S(s));
 }
 
+// ---------------------------------------------------------------------------
+// ModRaise (bootstrapping step 1): read a ciphertext modulo q_0 and
+// re-interpret its centred coefficients modulo q_0..q_level_out.  The result
+// encrypts t = m + q_0 I for a small integer polynomial I.
+__global__ void k_modraise_conv(const u64* r, u64* out, int n, int L, int nl, Tables tb) {
+    pdl_begin();
+    // r: [polys][N] coefficient form mod q_0;  out: [polys][L][N], limbs 0..nl-1 written
+    const int it = blockIdx.y;
+    const u64 q0 = tb.q[0], half = q0 >> 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const u64 v = r[(size_t)it * n + i];
+        const bool neg = v > half;
+        const u64 m = neg ? q0 - v : v;  // centred magnitude
+        for (int p = 0; p < nl; p++) {
+            const u64 q = tb.q[p];
+            const u64 mr = m % q;
+            out[((size_t)it * L + p) * n + i] = neg ? neg_mod(mr, q) : mr;
+        }
+    }
+}
+
+extern "C" int helr_mod_raise(helr_ctx* c, const uint64_t* a, uint64_t* out, int count, int level_out, void* sv) {
+    clear_stale_error("helr_mod_raise");
+    if (level_out < 0 || level_out >= c->L) { set_error("bad level"); return HELR_EINVAL; }
+    cudaStream_t s = S(sv);
+    const int n = c->n, L = c->L;
+    int chunk = (int)(c->ws_words / ((size_t)2 * n));
+    if (chunk < 1) { set_error("workspace too small"); return HELR_ENOMEM; }
+    for (int b0 = 0; b0 < count; b0 += chunk) {
+        const int nb = count - b0 < chunk ? count - b0 : chunk;
+        const int items = 2 * nb;  // polynomials
+        const u64* ab = (const u64*)a + (size_t)b0 * 2 * L * n;
+        u64* ob = (u64*)out + (size_t)b0 * 2 * L * n;
+        u64* r = c->ws;  // [items][N]
+        {
+            LimbMap m; m.count = 1; m.off[0] = 0; m.prime[0] = 0;
+            LdPolyLimb ld{ab, 2ll * L * n, (long long)L * n};
+            StBuf st{r, (long long)n, m, n};
+            ntt_launch<true>(c, ld, st, r, n, m, items, s);
+            CHECK_LAUNCH("mod_raise intt");
+        }
+        dim3 g1(blocks_for(n, 256), items);
+        {
+            ProfScope ps(PROF_RESCALE, 8.0 * n * items * (2 + level_out), s);
+            launch_pdl(k_modraise_conv, g1, dim3(256), 0, s, (const u64*)r, ob, n, L, level_out + 1, c->t);
+            CHECK_KERNEL("mod_raise conv");
+        }
+        LimbMap m = limb_range(0, level_out + 1);
+        ntt_buffers<false>(c, ob, (long long)L * n, ob, (long long)L * n, m, items, s);
+        CHECK_LAUNCH("mod_raise ntt");
+    }
+    return HELR_OK;
+}
+
 struct LinArgs {
     const u64* x[4];
     long long xs[4];

@@ -194,6 +194,9 @@ class CkksParams:
     cbd_eta: int = 21
     secret_hw: int = 64
     psi: tuple = field(default=(), compare=False)
+    # bootstrappable chains (bootstrap.bootstrap_ring): number of working
+    # levels below the bootstrapping levels; 0 = the whole chain is working levels
+    work_levels: int = 0
 
     def __post_init__(self):
         if not 2 <= self.log_n <= 17:
@@ -210,6 +213,8 @@ class CkksParams:
                 raise ValueError(f"{x} is not an NTT-friendly prime < 2**61 for N=2**{self.log_n}")
         if len(set(self.q) | set(self.p)) != len(self.q) + len(self.p):
             raise ValueError("primes must be distinct")
+        if not 0 <= self.work_levels < len(self.q):
+            raise ValueError(f"work_levels must be in [0, {len(self.q)}), got {self.work_levels}")
         if not 0 < self.cbd_eta <= 32:
             raise ValueError(f"cbd_eta must be in [1, 32], got {self.cbd_eta}")
         if not self.psi:
@@ -271,7 +276,10 @@ class CkksParams:
 
     @property
     def top_level(self) -> int:
-        return self.L - 1
+        """The working top: the level of fresh encryptions and of refreshed
+        ciphertexts.  Equal to L - 1 unless the chain reserves bootstrapping
+        levels above it (``work_levels``)."""
+        return self.work_levels if self.work_levels else self.L - 1
 
     def digits(self, level: int) -> int:
         """Number of key-switching digits in use at ``level`` (level+1 limbs)."""
@@ -283,9 +291,12 @@ class CkksParams:
         Delta_{l-1} = Delta_l**2 / q_l (so ct x ct products of canonical
         operands land exactly on the next canonical scale)."""
         s = [0.0] * self.L
-        s[self.L - 1] = float(2 ** self.scale_bits)
-        for lvl in range(self.L - 1, 0, -1):
+        top = self.top_level
+        s[top] = float(2 ** self.scale_bits)
+        for lvl in range(top, 0, -1):
             s[lvl - 1] = s[lvl] * s[lvl] / float(self.q[lvl])
+        # bootstrapping levels (above the working top) have no canonical
+        # scale: bootstrap.Bootstrapper tracks its own labels there
         return tuple(s)
 
     def he_params(self, noise_sigma: float = 1e-7, seed: int = 0) -> HeParams:
@@ -296,7 +307,7 @@ class CkksParams:
         enctrain.py:337); it is a nominal figure, the real noise is the
         CKKS error.
         """
-        return HeParams(log_n=self.log_n, log_q=self.scale_bits * self.L,
+        return HeParams(log_n=self.log_n, log_q=self.scale_bits * (self.top_level + 1),
                         log_delta=self.scale_bits, log_delta_c=self.scale_bits,
                         noise_sigma=noise_sigma, seed=seed)
 
