@@ -174,7 +174,7 @@ class BootstrapConfig:
     double_angles: int = 3
     degree: int = 63
     baby_log: int = 3          # Paterson-Stockmeyer baby step 2^baby_log
-    boot_bits: int = 55        # EvalMod working scale
+    boot_bits: int = 59        # EvalMod working scale: its rescale noise, amplified by K q_0 / scale_in, sets the precision
     min_ratio_bits: float = 11.5  # refuse inputs with q_0 / scale below 2^this (sine linearity)
 
     def __post_init__(self):
@@ -288,7 +288,7 @@ class Bootstrapper:
     ``ring`` supplies the primitives (names as in the C ABI): ``add``, ``sub``,
     ``add_const``, ``mul_const``, ``mul_plain``, ``encode_plain``,
     ``rescale``, ``mul`` (relinearise + rescale), ``rotate`` (by Galois
-    element), ``imul``, ``mod_raise``, ``cat``; buffers are opaque.
+    element), ``imul``, ``mod_raise``, ``cat``, ``split``; buffers are opaque.
     """
 
     def __init__(self, ring, cfg: Optional[BootstrapConfig] = None):
@@ -504,7 +504,8 @@ class Bootstrapper:
         v = self._eval_mod(u)
         # sin(2 pi t / q_0) ~ 2 pi m / q_0: re-label so the value is m / scale
         v = _Ct(v.buf, v.level, v.scale * 2.0 * np.pi * scale / q0)
-        w = ring.add(v.buf[0:1], ring.imul(v.buf[1:2], v.level), v.level)
+        v_re, v_im = ring.split(v.buf, 2)
+        w = ring.add(v_re, ring.imul(v_im, v.level), v.level)
         y = _Ct(w, v.level, v.scale)
         # (4) SlotToCoeff, landing on the canonical scale of the working top
         s_in, s_out = y.scale, self.out_scale
@@ -590,3 +591,6 @@ class GpuRing:
 
     def cat(self, bufs):
         return self._torch.cat(list(bufs), dim=0).contiguous()
+
+    def split(self, buf, parts: int):
+        return [c.contiguous() for c in self._torch.chunk(buf, parts, dim=0)]

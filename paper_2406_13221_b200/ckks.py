@@ -98,7 +98,15 @@ class GpuContext:
     COUNTER_KEYS = ("enc", "dec", "add", "cadd", "mul", "cmul", "imul", "rotate", "bootstrap")
 
     def __init__(self, ckks: CkksParams, seed: Optional[int] = None, noise_sigma: float = 1e-7,
-                 device: Optional[str] = None, max_batch: int = 8):
+                 device: Optional[str] = None, max_batch: int = 8, bootstrap: str = "refresh",
+                 bootstrap_config=None):
+        if bootstrap not in ("refresh", "ckks"):
+            raise ValueError(f"bootstrap must be 'refresh' or 'ckks', got {bootstrap!r}")
+        if bootstrap == "ckks" and not ckks.work_levels:
+            raise ValueError("bootstrap='ckks' needs a chain with bootstrapping levels (bootstrap.bootstrap_ring)")
+        self.bootstrap_mode = bootstrap
+        self._bootstrap_config = bootstrap_config
+        self._bootstrapper = None
         if not torch.cuda.is_available():
             raise _lib.NativeLibraryError("GpuContext needs a CUDA device (no CPU fallback)")
         self.ckks = ckks
@@ -430,13 +438,28 @@ class GpuContext:
         self.counters["add"] += 1
         return self._rotate(a, k, accumulate=True)
 
+    def bootstrapper(self):
+        """The real-bootstrapping circuit bound to this context (bootstrap='ckks')."""
+        if self._bootstrapper is None:
+            from .bootstrap import Bootstrapper, GpuRing
+
+            self._bootstrapper = Bootstrapper(GpuRing(self), self._bootstrap_config)
+        return self._bootstrapper
+
     def bootstrap(self, ct: GpuCiphertext) -> GpuCiphertext:
-        """Refresh STAND-IN (not bootstrapping): decrypt through q_0 with the
-        secret key, rescale the integer message to the top-level scale and
-        re-encrypt at the top level (hesim.py:228-236 semantics: level back
-        to log_q, slots preserved)."""
+        """hesim.py:228-236 semantics: level back to the working top, slots
+        preserved, counter bumped.
+
+        ``bootstrap='ckks'``: real CKKS bootstrapping (bootstrap.Bootstrapper:
+        ModRaise, CoeffToSlot, EvalMod, SlotToCoeff; public evaluation keys
+        only).  ``bootstrap='refresh'`` (default): the refresh STAND-IN (not
+        bootstrapping) — decrypt through q_0 with the secret key, rescale the
+        integer message to the top-level scale and re-encrypt at the top."""
         self.counters["bootstrap"] += 1
         ck = self.ckks
+        if self.bootstrap_mode == "ckks":
+            out, lvl, scale = self.bootstrapper().bootstrap(ct.data.unsqueeze(0).contiguous(), ct.level, ct.scale)
+            return self._wrap(out[0], lvl, scale, ct.boot_count + 1)
         top = ck.top_level
         target = ck.level_scales[top]
         ratio = target / ct.scale

@@ -46,7 +46,11 @@ struct HoistArgs {
     const u64* pm_sh;
 };
 
-template <int ND, int NB, bool DBL>
+// FULL: the chunk holds all NB ciphertexts (uniform per CTA), so the step
+// loop has no per-ciphertext branches: one basic block in which the prefetch
+// of step t + S - 1 is written piecewise between the multiply-accumulate
+// groups of step t.
+template <int ND, int NB, bool DBL, bool FULL>
 __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs& A, const Tables& tb) {
     const u64* __restrict__ ext = A.ext;
     const long long ext_item_stride = A.ext_item_stride, ext_digit_stride = A.ext_digit_stride;
@@ -73,27 +77,33 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
     const size_t kds = (size_t)2 * LK * n;
     auto slot = [&](int stage, int w) -> u64* { return hsm + ((size_t)(stage * W + w) * HOIST_T + tid); };
     const unsigned ei = 2u * (unsigned)brv_dev(i, log_n) + 1u;  // Galois index of this coefficient
-    auto issue = [&](int t) {
-        if (t < hk.nsteps) {
-            const int stage = t % S;
-            const int src = galois_perm_e(ei, (u64)hk.gal[t], log_n);
-            const u64* kt = hk.key[t];
+    // prefetch of step t in NB pieces: piece b copies ciphertext b's permuted
+    // digit words and a share of the 2 ND key words; the last piece commits
+    auto issue_piece = [&](int t, int b, int& src) {
+        // past the last step the prefetch re-reads the last step's words into
+        // a stage that was already consumed (harmless, L2 hits): no branch,
+        // so the whole step stays one basic block
+        const int stage = t % S;
+        const int tc = t < hk.nsteps ? t : hk.nsteps - 1;
+        if (b == 0) src = galois_perm_e(ei, (u64)hk.gal[tc], log_n);
+        const u64* kt = hk.key[tc];
 #pragma unroll
-            for (int j = 0; j < ND; j++) {
-                cp_async8(slot(stage, j), kt + (size_t)j * kds + k0off);
-                cp_async8(slot(stage, ND + j), kt + (size_t)j * kds + k1off);
-            }
-#pragma unroll
-            for (int b = 0; b < NB; b++) {
-                if (b < nb) {
-#pragma unroll
-                    for (int j = 0; j < ND; j++)
-                        cp_async8(slot(stage, 2 * ND + b * ND + j),
-                                  xb + (size_t)b * ext_item_stride + (size_t)j * ext_digit_stride + src);
-                }
-            }
+        for (int w = b; w < 2 * ND; w += NB) {
+            const int j = w < ND ? w : w - ND;
+            cp_async8(slot(stage, w), kt + (size_t)j * kds + (w < ND ? k0off : k1off));
         }
-        cp_async_commit();  // empty groups keep the wait count uniform
+        if (FULL || b < nb) {
+#pragma unroll
+            for (int j = 0; j < ND; j++)
+                cp_async8(slot(stage, 2 * ND + b * ND + j),
+                          xb + (size_t)b * ext_item_stride + (size_t)j * ext_digit_stride + src);
+        }
+        if (b == NB - 1) cp_async_commit();
+    };
+    auto issue = [&](int t) {
+        int src = 0;
+#pragma unroll
+        for (int b = 0; b < NB; b++) issue_piece(t, b, src);
     };
     using Acc = typename std::conditional<DBL, dacc, macc>::type;
     Acc a0[NB], a1[NB];
@@ -105,24 +115,40 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
 #pragma unroll
     for (int t = 0; t < S - 1; t++) issue(t);
     int run = 0;
+    static_assert(S >= 2, "the prefetch needs at least two stages");
     for (int t = 0; t < hk.nsteps; t++) {
-        issue(t + S - 1);
-        cp_async_wait<S - 1>();
+        // step t's words have landed (step t + 1 may still be in flight); they
+        // are read into registers first and step t + S - 1 is issued AFTER
+        // that, so its address arithmetic and cp.async instructions sit
+        // between this step's fp64 multiply-accumulates in the instruction
+        // stream (the fp64 pipe takes one instruction every other cycle; the
+        // integer work fills the gaps) instead of forming a separate phase
+        cp_async_wait<S - 2>();
         const int stage = t % S;
+        u64 kw[2 * ND], dw[NB * ND];
+#pragma unroll
+        for (int j = 0; j < 2 * ND; j++) kw[j] = *slot(stage, j);
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+#pragma unroll
+            for (int j = 0; j < ND; j++) dw[b * ND + j] = (FULL || b < nb) ? *slot(stage, 2 * ND + b * ND + j) : 0;
+        }
+        int nsrc = 0;
         if constexpr (DBL) {
             double k0h[ND], k0l[ND], k1h[ND], k1l[ND];
 #pragma unroll
             for (int j = 0; j < ND; j++) {
-                split21(*slot(stage, j), k0h[j], k0l[j]);
-                split21(*slot(stage, ND + j), k1h[j], k1l[j]);
+                split21(kw[j], k0h[j], k0l[j]);
+                split21(kw[ND + j], k1h[j], k1l[j]);
             }
 #pragma unroll
             for (int b = 0; b < NB; b++) {
-                if (b < nb) {
+                issue_piece(t + S - 1, b, nsrc);
+                if (FULL || b < nb) {
 #pragma unroll
                     for (int j = 0; j < ND; j++) {
                         double uh, ul;
-                        split21_d(__longlong_as_double((long long)*slot(stage, 2 * ND + b * ND + j)), uh, ul);
+                        split21_d(__longlong_as_double((long long)dw[b * ND + j]), uh, ul);
                         mac_d(a0[b], uh, ul, k0h[j], k0l[j]);
                         mac_d(a1[b], uh, ul, k1h[j], k1l[j]);
                     }
@@ -138,20 +164,15 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
                 run = 0;
             }
             run++;
-            u64 k0[ND], k1[ND];
-#pragma unroll
-            for (int j = 0; j < ND; j++) {
-                k0[j] = *slot(stage, j);
-                k1[j] = *slot(stage, ND + j);
-            }
 #pragma unroll
             for (int b = 0; b < NB; b++) {
-                if (b < nb) {
+                issue_piece(t + S - 1, b, nsrc);
+                if (FULL || b < nb) {
 #pragma unroll
                     for (int j = 0; j < ND; j++) {
-                        const u64 u = *slot(stage, 2 * ND + b * ND + j);
-                        mac_split(a0[b], u, k0[j]);
-                        mac_split(a1[b], u, k1[j]);
+                        const u64 u = dw[b * ND + j];
+                        mac_split(a0[b], u, kw[j]);
+                        mac_split(a1[b], u, kw[ND + j]);
                     }
                 }
             }
@@ -215,10 +236,15 @@ __global__ void __launch_bounds__(HOIST_T, HELR_HOIST_MINB) k_ks_inner_hoisted(H
     pdl_begin();
     const int e = blockIdx.y;
     const int p = e < A.nl ? e : A.L + (e - A.nl);
-    if (tb.q[p] < NTT_DBL_BOUND)  // uniform per CTA (one limb per CTA)
-        hoist_body<ND, NB, true>(hk, A, tb);
-    else
-        hoist_body<ND, NB, false>(hk, A, tb);
+    const int chunk = blockIdx.x % A.nchunks;
+    const bool full = A.B - chunk * NB >= NB;
+    if (tb.q[p] < NTT_DBL_BOUND) {  // uniform per CTA (one limb per CTA)
+        if (full) hoist_body<ND, NB, true, true>(hk, A, tb);
+        else hoist_body<ND, NB, true, false>(hk, A, tb);
+    } else {
+        if (full) hoist_body<ND, NB, false, true>(hk, A, tb);
+        else hoist_body<ND, NB, false, false>(hk, A, tb);
+    }
 }
 
 // ---- bulk-copy pipeline variant ---------------------------------------------

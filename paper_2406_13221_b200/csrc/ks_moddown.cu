@@ -9,6 +9,15 @@
 #include "conv.cuh"
 
 // ModDown conversion: mdc[b][poly][i] = sum_k [a_k * phinv_k]_{p_k} * phmod[k][i] mod q_i
+// The conversion kernels write fp64 limbs as raw doubles (read by the NTT with
+// in_raw) only when every source prime is below 2^41; with a wide source they
+// write canonical residues for every limb and the NTT must read them as such.
+static inline bool specials_fp64(const helr_ctx* c) {
+    for (int k = 0; k < c->K; k++)
+        if (c->primes[c->L + k] >= NTT_DBL_BOUND) return false;
+    return true;
+}
+
 // Centred conversion (see oracle oc_moddown_convert): subtract r*P with
 // r = round(sum_k y_k / p_k) evaluated in IEEE double without contraction,
 // so the ModDown error is the zero-mean rounding of x / P.
@@ -91,6 +100,8 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
                 s1 = add_mod(s1, shoup(z1[k], w, ws, q), q);
             }
         }
+        // canonical residues: with a wide source prime no limb takes the fp64
+        // branch above and the host launches the NTT without in_raw
         st2(mp + (size_t)p * n + i, sub_mod(s0, shoup(rr0, pm[p], pm_sh[p], q), q),
             sub_mod(s1, shoup(rr1, pm[p], pm_sh[p], q), q));
     }
@@ -178,7 +189,7 @@ int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const KsWs& 
         st.add_p = ep.add_p; st.p_is = ep.add_p_stride;
         st.ngal = ep.add_p ? ep.ngal : 0;
         for (int t = 0; t < HELR_MAX_HOIST; t++) st.gal[t] = ep.gal[t];
-        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s, 1);
+        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s, specials_fp64(c) ? 1 : 0);
         CHECK_LAUNCH("ks moddown ntt+final");
     }
     return HELR_OK;
@@ -267,6 +278,7 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
                 s1 = add_mod(s1, shoup(z1[k], w, ws, q), q);
             }
         }
+        // canonical residues (see k_moddown_conv)
         st2(mp + (size_t)p * n + i, sub_mod(s0, shoup(rr0, mt.mm[p], mt.mms[p], q), q),
             sub_mod(s1, shoup(rr1, mt.mm[p], mt.mms[p], q), q));
     }
@@ -333,7 +345,7 @@ int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, int B, co
     {
         LdBuf ld{w.mdc, w.mdc_s, mq, n};
         const StCombine st = st_combine(c, out, os, (long long)L * n, w.acc, w.acc_s, (long long)ne * n, mt.mi, mt.mis, l);
-        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s, 1);
+        ntt_launch<false>(c, ld, st, w.mdc, w.mdc_s, mq, B, s, specials_fp64(c) && c->primes[l] < NTT_DBL_BOUND ? 1 : 0);
         CHECK_LAUNCH("mdr ntt+final");
     }
     return HELR_OK;

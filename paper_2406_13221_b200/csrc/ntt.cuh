@@ -292,7 +292,14 @@ constexpr u64 NTT_DBL_BOUND = 1ull << 41;
 // (bx, li, z) = sub-transform tile, limb index in map, batch item.  S2 =
 // log N - LOG_T (column passes: the element stride is 2^S2, a compile-time
 // constant so every register's address is an immediate offset).
-template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, bool DBL, class Ld, class St>
+// PRE: the CTA's input tile is already in `sm` (placed there by a TMA bulk
+// tensor copy, ntt_tma.cuh): column tiles dense as [T][COLS], row tiles as
+// [T * COLS / 16][16] words with the 128-byte hardware swizzle.  The tile is
+// consumed into registers, then the same buffer serves the padded exchange.
+__device__ __forceinline__ int swz128(int e) {  // word index -> swizzled word index
+    return (e & ~15) | (((((e >> 1) ^ (e >> 4)) & 7) << 1)) | (e & 1);
+}
+template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, bool DBL, class Ld, class St, bool PRE = false>
 __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
                                          const NttPassArgs& a, u64* sm, const int bx, const int li, const int z) {
     using S = NttShape<LOG_T, LOG_R>;
@@ -381,7 +388,23 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                             : ((g * LOG_R < LOG_T - LOG_R) ? g * LOG_R : LOG_T - LOG_R);
         const int base = spread_index(s, lo, LOG_R);
         if (g == 0) {
-            if constexpr (!IS_COL && has_tile<Ld>::value) {
+            if constexpr (PRE) {
+                static_assert(NG >= 2, "preloaded tiles need an exchange");
+                if constexpr (IS_COL) {
+#pragma unroll
+                    for (int i = 0; i < R; i++) x[i] = in_v(sm[(base + (i << lo)) * COLS + cc]);
+                } else if (lo == 0) {
+#pragma unroll
+                    for (int i = 0; i < R; i += 2) {
+                        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sm + swz128(cc * T + base + i));
+                        x[i] = in_v(v.x);
+                        x[i + 1] = in_v(v.y);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < R; i++) x[i] = in_v(sm[swz128(cc * T + base + (i << lo))]);
+                }
+            } else if constexpr (!IS_COL && has_tile<Ld>::value) {
                 if (lo == 0) {
                     // coalesced prologue: the CTA's T * COLS contiguous inputs
                     // through shared memory (each thread then takes R in a row)
@@ -508,6 +531,9 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                 for (int i = 0; i < R; i++) ST(base + (i << lo), y[i]);
             }
         } else {
+            if constexpr (PRE) {
+                if (g == 0) __syncthreads();  // every thread has consumed the preloaded tile
+            }
 #pragma unroll
             for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = to_sm(x[i]);
             __syncthreads();
@@ -583,6 +609,8 @@ struct StBuf {
     }
 };
 
+#include "ntt_tma.cuh"
+
 // ---- host-side dispatch ----------------------------------------------------
 // Launch one NTT (forward or inverse) over `count` items x map.count limbs.
 // The first pass reads through `ld`, the last pass writes through `st`; with
@@ -616,6 +644,12 @@ static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const 
     const int cols = subs < COLS ? subs : COLS;  // tiny rings: fewer sub-transforms than COLS
     NttPassArgs a{log_n, st0, final_out, raw_in, raw_out, dbl_out};
     count_launches(1);
+    // large launches at N = 2^16 from plain buffers: persistent CTAs whose next
+    // tile arrives by TMA while the current one computes (ntt_tma.cuh)
+    if constexpr (std::is_same<Ld, LdBuf>::value && LOG_T == ntma::LOG_T && COLS == ntma::COLS &&
+                  (!IS_COL || S2 == ntma::LOG_N - ntma::LOG_T)) {
+        if (ntma::usable(log_n, ld, map, count) && ntma::launch<IS_COL, INV>(ld, st, tb, map, a, count, s)) return;
+    }
     if (cols == COLS) {
         const long long full = (long long)(subs / COLS) * map.count * count;
         if (COLS_S < COLS && full < NTT_SMALL_GRID && log_n >= 12) {

@@ -213,6 +213,14 @@ class FusedTrainer:
         # so the refresh's fresh encryption noise is negligible, below 2^50 so
         # the row-start mask still encodes at >= 2^35
         self.refresh_bits = refresh_bits
+        # bootstrap='ckks' contexts (real bootstrapping, bootstrap.py): the sine
+        # of EvalMod is linear only for |message| << q_0, so W', V' reach the
+        # bottom level two bits lower (q_0 / scale = 2^12), and the refreshed
+        # W, V come back at the working top's canonical scale
+        self.real_bootstrap = getattr(ctx, "bootstrap_mode", "refresh") == "ckks"
+        self.out_bits = OUT_SCALE_BITS - 2 if self.real_bootstrap else OUT_SCALE_BITS
+        if self.real_bootstrap:
+            self.refresh_bits = ctx.ckks.scale_bits
         self.layout: BlockLayout = plan_layout(ds.n_samples, ds.n_features, ctx.params, rows_per_block)
         lay = self.layout
         self.rows = blocks_per_batch
@@ -296,7 +304,7 @@ class FusedTrainer:
         # product G * B̄ stay >= 2^33 (relative rounding <= 2^-34)
         s_b0 = s_top / float(np.max(np.abs(bb)))
         trial = plan_iteration(ck, top, 2.0 ** self.refresh_bits, 2.0 ** self.refresh_bits, s_top, s_b0, self.qpoly,
-                               1.0, 0.37)
+                               1.0, 0.37, self.out_bits)
         ca_bits = math.log2(min(abs(trial.ints[5]), abs(trial.ints[8])))
         self.bbar_extra_bits = int(max(0, min(BBAR_EXTRA_BITS, math.floor(ca_bits - 33))))
         self.s_b = s_b0 * 2.0 ** self.bbar_extra_bits
@@ -404,8 +412,20 @@ class FusedTrainer:
         return True
 
     def refresh(self):
-        """Refresh stand-in on W and V (NOT bootstrapping; see helr_refresh)."""
+        """Bring W and V back to the working top: real CKKS bootstrapping of
+        the 2C ciphertexts in one batched circuit when the context was made
+        with bootstrap='ckks' (bootstrap.Bootstrapper, evaluation keys only),
+        else the refresh stand-in (NOT bootstrapping; see helr_refresh)."""
         ck = self.ck
+        if self.real_bootstrap:
+            if abs(self.s_w / self.s_v - 1.0) > 1e-12:
+                raise ValueError("W and V must share a scale to bootstrap as one batch")
+            out, lvl, scale = self.ctx.bootstrapper().bootstrap(self.wv, self.level, self.s_w)
+            self.ctx.counters["bootstrap"] += self.wv.shape[0]
+            self.wv.copy_(out)
+            self.level = lvl
+            self.s_w = self.s_v = scale
+            return
         top = ck.top_level
         target = float(2 ** self.refresh_bits)
         ratio = target / self.s_w
@@ -535,7 +555,8 @@ class FusedTrainer:
             b = 0
             gamma_rows = self.ds.n_samples
         lr, eta, gamma, mult = self.step_scalars(self.t, gamma_rows)
-        plan = plan_iteration(self.ck, self.level, self.s_w, self.s_v, self.s_z, self.s_b, self.qpoly, mult, eta)
+        plan = plan_iteration(self.ck, self.level, self.s_w, self.s_v, self.s_z, self.s_b, self.qpoly, mult, eta,
+                              self.out_bits)
         self._upload_consts(plan)
         nbt = self.n_batches
         if self.mode == "mini_batch":

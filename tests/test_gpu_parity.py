@@ -40,6 +40,9 @@ RINGS = {
     # integer (Shoup / 128-bit accumulator) path; dnum 1 and 3, L 16 and 24
     "sweep_i50": CkksParams.generate(log_n=14, n_q=16, dnum=1, scale_bits=50, p_bits=60),
     "sweep_l24": CkksParams.generate(log_n=14, n_q=24, dnum=3, scale_bits=55, p_bits=60),
+    # 60-bit special primes above 40-bit scaling primes: the ModDown conversions
+    # take the integer path but feed fp64 limbs (the bootstrapping chains' mix)
+    "mixed_p60": CkksParams.generate(log_n=12, n_q=6, dnum=2, p_bits=60),
 }
 
 
