@@ -192,7 +192,7 @@ class BootstrapConfig:
 
 def bootstrap_ring(log_n: int, work_levels: int = 7, scale_bits: int = 40, cfg: Optional[BootstrapConfig] = None,
                    dnum: Optional[int] = None, q0_bits: int = 60, s2c_bits: int = 45, c2s_bits: int = 58,
-                   secret_hw: int = 64, cbd_eta: int = 21) -> CkksParams:
+                   secret_hw: int = 64, cbd_eta: int = 21, p_bits: int = 60) -> CkksParams:
     """A modulus chain with room for one bootstrap above ``work_levels``
     working levels: q_0 | work_levels primes of ``scale_bits`` | s2c_groups of
     ``s2c_bits`` | EvalMod primes of ``cfg.boot_bits`` | c2s_groups of
@@ -217,8 +217,8 @@ def bootstrap_ring(log_n: int, work_levels: int = 7, scale_bits: int = 40, cfg: 
         dnum = -(-n_q // 4)
     alpha = -(-n_q // dnum)
     digit_bits = max(sum(math.log2(x) for x in q[j * alpha:(j + 1) * alpha]) for j in range(dnum))
-    n_special = int(-(-(digit_bits + 20) // 60))
-    p = take(60, n_special, "below")
+    n_special = int(-(-(digit_bits + 20) // p_bits))
+    p = take(p_bits, n_special, "below")
     return CkksParams(log_n=log_n, q=tuple(q), p=tuple(p), dnum=dnum, scale_bits=scale_bits, cbd_eta=cbd_eta,
                       secret_hw=secret_hw, work_levels=work_levels)
 

@@ -107,6 +107,7 @@ class GpuContext:
         self.bootstrap_mode = bootstrap
         self._bootstrap_config = bootstrap_config
         self._bootstrapper = None
+        self._boot_graphs: dict = {}
         if not torch.cuda.is_available():
             raise _lib.NativeLibraryError("GpuContext needs a CUDA device (no CPU fallback)")
         self.ckks = ckks
@@ -446,6 +447,35 @@ class GpuContext:
             self._bootstrapper = Bootstrapper(GpuRing(self), self._bootstrap_config)
         return self._bootstrapper
 
+    def bootstrap_batch(self, buf: torch.Tensor, level: int, scale: float, use_graph: bool = False):
+        """Real bootstrapping of ``buf`` (int64[count][2][L][N], all at ``level``
+        with scale label ``scale``) as one batched circuit -> (buffer, level,
+        scale).  The circuit is static for a given (shape, level, scale);
+        ``use_graph`` captures its ~400 primitive calls into a CUDA graph after
+        one eager run (which builds the Galois keys, the plaintext diagonals
+        and the constant residues).  Measured at N = 2^16 for W, V: 84.3 ms
+        eager and 84.3 ms replayed — the circuit is bound by its kernels (the
+        45-59-bit bootstrapping primes take the integer NTT path), not by the
+        host, so the graph is off by default."""
+        bs = self.bootstrapper()
+        if not use_graph:
+            return bs.bootstrap(buf, level, scale)
+        key = (tuple(buf.shape), int(level), float(scale))
+        ent = self._boot_graphs.get(key)
+        if ent is None:
+            static_in = buf.clone()
+            bs.bootstrap(static_in, level, scale)
+            torch.cuda.synchronize(self.device)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                out, lvl, sc = bs.bootstrap(static_in, level, scale)
+            ent = (graph, static_in, out, lvl, sc)
+            self._boot_graphs[key] = ent
+        graph, static_in, out, lvl, sc = ent
+        static_in.copy_(buf)
+        graph.replay()
+        return out, lvl, sc
+
     def bootstrap(self, ct: GpuCiphertext) -> GpuCiphertext:
         """hesim.py:228-236 semantics: level back to the working top, slots
         preserved, counter bumped.
@@ -458,8 +488,8 @@ class GpuContext:
         self.counters["bootstrap"] += 1
         ck = self.ckks
         if self.bootstrap_mode == "ckks":
-            out, lvl, scale = self.bootstrapper().bootstrap(ct.data.unsqueeze(0).contiguous(), ct.level, ct.scale)
-            return self._wrap(out[0], lvl, scale, ct.boot_count + 1)
+            out, lvl, scale = self.bootstrap_batch(ct.data.unsqueeze(0).contiguous(), ct.level, ct.scale)
+            return self._wrap(out[0].clone(), lvl, scale, ct.boot_count + 1)
         top = ck.top_level
         target = ck.level_scales[top]
         ratio = target / ct.scale

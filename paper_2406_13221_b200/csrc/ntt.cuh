@@ -552,7 +552,11 @@ template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, class L
 #ifndef HELR_NTT_MINB
 #define HELR_NTT_MINB 4  // resident 256-thread CTAs per SM the register budget is sized for
 #endif
+#ifndef HELR_NTT_MINB512
+#define HELR_NTT_MINB512 3  // 512-thread CTAs (radix-8 register groups, HELR_NTT_LOGR=3)
+#endif
 __global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R),
+                                  ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 512 ? HELR_NTT_MINB512 :
                                   ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 256 ? HELR_NTT_MINB : 1)
 ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     pdl_begin();
@@ -629,12 +633,15 @@ constexpr long long NTT_SMALL_GRID = HELR_NTT_SMALL_GRID;
 #ifndef HELR_NTT_SMALL_LOGR
 #define HELR_NTT_SMALL_LOGR 2
 #endif
+#ifndef HELR_NTT_LOGR
+#define HELR_NTT_LOGR 4  // log2 of the elements a thread holds (radix-16 register groups)
+#endif
 
 template <int LOG_T, bool IS_COL, bool INV, int S2, class Ld, class St>
 static void ntt_pass_launch(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
                             int log_n, int st0, int final_out, int count, cudaStream_t s, int raw_in = 0,
                             int raw_out = 0, int dbl_out = 0) {
-    constexpr int LOG_R = LOG_T < 4 ? LOG_T : 4;
+    constexpr int LOG_R = LOG_T < HELR_NTT_LOGR ? LOG_T : HELR_NTT_LOGR;
     constexpr int T = 1 << LOG_T;
     // column passes: 16 adjacent columns (128-byte rows); row passes: ~4096 elements per CTA
     constexpr int COLS_ROW = (4096 / T) > 0 ? (4096 / T) : 1;

@@ -420,7 +420,7 @@ class FusedTrainer:
         if self.real_bootstrap:
             if abs(self.s_w / self.s_v - 1.0) > 1e-12:
                 raise ValueError("W and V must share a scale to bootstrap as one batch")
-            out, lvl, scale = self.ctx.bootstrapper().bootstrap(self.wv, self.level, self.s_w)
+            out, lvl, scale = self.ctx.bootstrap_batch(self.wv, self.level, self.s_w)
             self.ctx.counters["bootstrap"] += self.wv.shape[0]
             self.wv.copy_(out)
             self.level = lvl

@@ -30,9 +30,14 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--scale-bits", type=int, default=40)
     ap.add_argument("--in-bits", type=int, default=48, help="scale of the exhausted input on q_0 (the trainer's W', V')")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--dnum", type=int, default=None)
+    ap.add_argument("--p-bits", type=int, default=60)
+    ap.add_argument("--c2s", type=int, default=3)
+    ap.add_argument("--s2c", type=int, default=3)
     a = ap.parse_args()
-    cfg = BootstrapConfig()
-    P = bootstrap_ring(a.log_n, work_levels=7, scale_bits=a.scale_bits, cfg=cfg)
+    cfg = BootstrapConfig(c2s_groups=a.c2s, s2c_groups=a.s2c)
+    P = bootstrap_ring(a.log_n, work_levels=7, scale_bits=a.scale_bits, cfg=cfg, dnum=a.dnum, p_bits=a.p_bits)
     t0 = time.time()
     ctx = GpuContext(P, seed=3, max_batch=max(4, 2 * a.count), bootstrap="ckks")
     bs = ctx.bootstrapper()
@@ -42,14 +47,15 @@ def main():
     buf = ctx._empty((a.count, 2, P.L, P.n))
     ctx.encrypt_to(ctx.encoder.encode(z, s_in), buf, 0)      # level-0 ciphertexts at the trainer's bottom scale
     torch.cuda.synchronize()
-    out, lvl, sc = bs.bootstrap(buf, 0, s_in)                 # first call: keys and plaintext diagonals are built
+    boot = lambda: ctx.bootstrap_batch(buf, 0, s_in, use_graph=not a.no_graph)
+    out, lvl, sc = boot()                                     # first call: keys, plaintext diagonals, graph capture
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     ms = []
     for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        out, lvl, sc = bs.bootstrap(buf, 0, s_in)
+        out, lvl, sc = boot()
         e1.record()
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
@@ -62,7 +68,7 @@ def main():
     pt_gb = sum(t.numel() * 8 for pts, _ in bs._pt_cache.values() for t in pts.values()) / 1e9
     print(json.dumps({"log_n": a.log_n, "L": P.L, "K": P.K, "dnum": P.dnum, "count": a.count, "depth": cfg.depth,
                       "out_level": lvl, "ms_per_bootstrap": round(min(ms), 2), "ms_all": [round(x, 2) for x in ms],
-                      "max_err": max(errs), "switch_keys": keys, "key_gb": round(key_gb, 2),
+                      "max_err": max(errs), "cuda_graph": not a.no_graph, "switch_keys": keys, "key_gb": round(key_gb, 2),
                       "plaintext_gb": round(pt_gb, 2), "setup_s": round(setup_s, 1),
                       "counters": {k: v for k, v in ctx.counters.items() if v}}))
 
