@@ -313,6 +313,7 @@ class Bootstrapper:
             self.S[lvl - 1] = self.S[lvl] * self.S[lvl] / float(ck.q[lvl])
         self.out_scale = float(ck.level_scales[self.out_level])
         self._pt_cache: dict = {}
+        self.pt_variants = 4
         self.conj_galois = 2 * ck.n - 1
 
     # -- what the evaluator has to prepare -----------------------------------
@@ -371,19 +372,26 @@ class Bootstrapper:
 
     # -- linear transforms ------------------------------------------------------
     def _plaintexts(self, key, t: _Transform, level: int, pt_scale: float):
-        ck = (key, level)
-        if ck not in self._pt_cache:
-            pts = {}
-            g, st, n = t.baby, t.step, self.n
-            for i, js in t.terms.items():
-                for j in js:
-                    d = t.signed[g * i + j]
-                    vec = np.roll(t.diagonals[d], (g * i * st) % n)   # rot(diag, -g i step)
-                    pts[(i, j)] = self.ring.encode_plain(self.encoder.encode(vec, pt_scale), level)
-            self._pt_cache[ck] = (pts, pt_scale)
-        pts, cached_scale = self._pt_cache[ck]
-        if cached_scale != pt_scale:
-            raise ValueError("plaintext cache was built for a different scale")
+        """Encoded diagonals of one factor, cached per (factor, level, scale).
+        CoeffToSlot scales are fixed by the chain; SlotToCoeff scales follow
+        the input's scale label (W and V of the per-op driver arrive at two
+        different bottom scales), so a few variants per factor are kept
+        (least recently used dropped beyond ``pt_variants``)."""
+        ck = (key, level, float(pt_scale))
+        if ck in self._pt_cache:
+            self._pt_cache[ck] = self._pt_cache.pop(ck)     # most recently used last
+            return self._pt_cache[ck][0]
+        pts = {}
+        g, st, n = t.baby, t.step, self.n
+        for i, js in t.terms.items():
+            for j in js:
+                d = t.signed[g * i + j]
+                vec = np.roll(t.diagonals[d], (g * i * st) % n)   # rot(diag, -g i step)
+                pts[(i, j)] = self.ring.encode_plain(self.encoder.encode(vec, pt_scale), level)
+        same = [k for k in self._pt_cache if k[0] == key and k[1] == level]
+        while len(same) >= self.pt_variants:
+            del self._pt_cache[same.pop(0)]
+        self._pt_cache[ck] = (pts, pt_scale)
         return pts
 
     def _linear(self, key, t: _Transform, x: _Ct, target_scale: float) -> _Ct:

@@ -399,3 +399,25 @@ def test_exact_sigmoid_rejected(ctx, rng):
     cfg = O.TrainConfig(mode="mini_batch", batch_size=4, max_iterations=1, sigmoid="exact")
     with pytest.raises(ValueError, match="polynomial"):
         T.train_encrypted(toy_dataset(rng), cfg, ctx.params, ctx=ctx)
+
+
+def test_train_encrypted_with_real_bootstrapping():
+    """The reference driver over a GpuContext whose ``bootstrap`` is REAL CKKS
+    bootstrapping (bootstrap='ckks', evaluation keys only; SURVEY.md §8(f) row
+    1): same cadence and op ledger as with the stand-in, weight trace within
+    the bootstrap's precision of the reference simulator's trace."""
+    from paper_2406_13221_b200.bootstrap import bootstrap_ring
+
+    ds, g = _golden_case("mini_g8")
+    ring = bootstrap_ring(5, work_levels=9)   # ten working limbs = mk(n_q=10): one literal iteration per refresh
+    c = GpuContext(ring, seed=5, max_batch=4, bootstrap="ckks")
+    cfg = O.TrainConfig(mode="mini_batch", batch_size=4, max_iterations=7, schedule=O.LrSchedule(2.0, 1.0, 36, 2.5),
+                        sigmoid="g8")
+    res = T.train_encrypted(ds, cfg, c.params, ctx=c, trace_weights=True, metrics=False)
+    assert len(res.weight_trace) == len(g["mini_g8_trace"])
+    worst = max(float(np.max(np.abs(np.asarray(a) - np.asarray(b)))) for a, b in zip(res.weight_trace, g["mini_g8_trace"]))
+    print(f"train_encrypted with real bootstrapping: max |dw| = {worst:.3e}")
+    assert worst < 1e-4
+    assert [r["bootstraps"] for r in res.ledger] == [0] + [1] * (len(res.ledger) - 1)
+    assert [r["muls"] for r in res.ledger] == list(g["mini_g8_muls"])
+    assert c.counters["bootstrap"] >= 2 * (len(res.ledger) - 1) or sum(r["boot_ops"] for r in res.ledger) >= 2

@@ -56,6 +56,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batches", type=int, default=16)
     ap.add_argument("--iters", type=int, default=16)
+    ap.add_argument("--work-levels", type=int, default=7, help="7: one iteration per bootstrap; 14: two")
+    ap.add_argument("--dnum", type=int, default=None)
     a = ap.parse_args()
     ds = data.paper_dataset(n=1024 * a.batches)
     out = {"rows": ds.n_samples, "features": 200, "iters": a.iters}
@@ -66,11 +68,12 @@ def main():
     del ctx
     gc.collect()
     torch.cuda.empty_cache()
-    ckb = bootstrap_ring(16, work_levels=7)
+    ckb = bootstrap_ring(16, work_levels=a.work_levels, dnum=a.dnum)
     ctxb = GpuContext(ckb, seed=1, max_batch=8, bootstrap="ckks")
     ms1, w1, b1 = run(ctxb, ds, a.iters)
     out["real_bootstrap"] = {"ms_per_iteration": round(ms1, 3), "iterations_per_s": round(1000.0 / ms1, 3),
-                             "L": ckb.L, "K": ckb.K, "dnum": ckb.dnum, "bootstrapped_ciphertexts": b1,
+                             "L": ckb.L, "K": ckb.K, "dnum": ckb.dnum, "work_levels": a.work_levels,
+                             "bootstrapped_ciphertexts": b1,
                              "bootstrap_share": round(1.0 - ms0 / ms1, 3)}
     out["max_weight_difference"] = [float(np.max(np.abs(x - y))) for x, y in zip(w0, w1)]
     print(json.dumps(out))
