@@ -9,10 +9,13 @@ with ``python -m paper_2406_13221_b200.build`` (or ``__graft_entry__.build()``).
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libhelr_ckks.so"
+# HELR_LIB: developer knob for A/B runs of differently built variants of the
+# same library (tools/build_variant.sh); never a different implementation
+LIB_PATH = Path(os.environ.get("HELR_LIB") or PKG / "libhelr_ckks.so")
 
 
 class NativeLibraryError(RuntimeError):

@@ -32,6 +32,14 @@
 #define HELR_NTT_EPI_UNROLL 4  // tile-epilogue pairs per thread in flight
 #endif
 constexpr int kNttEpiUnroll = HELR_NTT_EPI_UNROLL;
+#ifndef HELR_NTT_COLTW_SMEM
+#define HELR_NTT_COLTW_SMEM 1
+#endif
+constexpr bool kColTwSmem = HELR_NTT_COLTW_SMEM;
+#ifndef HELR_NTT_ROW_WARPSYNC
+#define HELR_NTT_ROW_WARPSYNC 1
+#endif
+constexpr bool kRowWarpSync = HELR_NTT_ROW_WARPSYNC;
 
 void count_launches(int k);
 
@@ -195,8 +203,36 @@ __device__ __forceinline__ double d2d_canon(double x, const DblC& c) {
 // more, start at an even index (the low bits of the register group's base
 // are zero above bit lo), so they load as 16-byte pairs, all issued before
 // the butterflies.
-template <int NW>
+#ifndef HELR_NTT_EXP
+#define HELR_NTT_EXP 0  // timing experiments only (wrong results), bit mask: 1 no twiddle loads, 2 no butterflies, 4 no global loads, 8 no global stores
+#endif
+template <int NW, bool SM = false>
 __device__ __forceinline__ void load_tw(double (&w)[NW], const double* __restrict__ W, int tb0) {
+#if HELR_NTT_EXP & 1
+    if constexpr (SM) {
+#pragma unroll
+        for (int j = 0; j < NW; j++) w[j] = 3.0 + j;
+        return;
+    }
+#endif
+    if constexpr (SM) {  // shared-memory table (column passes): plain loads, LDS after inlining
+        if constexpr (NW >= 2) {
+#pragma unroll
+            for (int j = 0; j < NW; j += 2) {
+                const double2 p = *reinterpret_cast<const double2*>(W + tb0 + j);
+                w[j] = p.x;
+                w[j + 1] = p.y;
+            }
+        } else {
+            w[0] = W[tb0];
+        }
+        return;
+    }
+#if HELR_NTT_EXP & 1
+#pragma unroll
+    for (int j = 0; j < NW; j++) w[j] = 3.0 + j;
+    return;
+#endif
     if constexpr (NW >= 2) {
 #pragma unroll
         for (int j = 0; j < NW; j += 2) {
@@ -208,10 +244,10 @@ __device__ __forceinline__ void load_tw(double (&w)[NW], const double* __restric
         w[0] = __ldg(W + tb0);
     }
 }
-template <int R, int H>
+template <int R, int H, bool SM = false>
 __device__ __forceinline__ void fwd_stage_d(double (&x)[R], const double* __restrict__ W, int tb0, const DblC& c) {
     double wv[R >> (H + 1)];
-    load_tw(wv, W, tb0);
+    load_tw<(R >> (H + 1)), SM>(wv, W, tb0);
 #pragma unroll
     for (int j = 0; j < (R >> (H + 1)); j++) {
         const double w = wv[j];
@@ -224,10 +260,10 @@ __device__ __forceinline__ void fwd_stage_d(double (&x)[R], const double* __rest
         }
     }
 }
-template <int R, int H>
+template <int R, int H, bool SM = false>
 __device__ __forceinline__ void inv_stage_d(double (&x)[R], const double* __restrict__ W, int tb0, const DblC& c) {
     double wv[R >> (H + 1)];
-    load_tw(wv, W, tb0);
+    load_tw<(R >> (H + 1)), SM>(wv, W, tb0);
 #pragma unroll
     for (int j = 0; j < (R >> (H + 1)); j++) {
         const double w = wv[j];
@@ -250,22 +286,22 @@ __device__ __forceinline__ void inv_last_stage_d(double (&x)[R], double ni, doub
         x[i + (1 << H)] = mulmod_d(__dsub_rn(u, v), wl, c);
     }
 }
-template <int R>
+template <int R, bool SM = false>
 __device__ __forceinline__ void fwd_stage_dh(int h, double (&x)[R], const double* W, int tb0, const DblC& c) {
     switch (h) {
-        case 0: fwd_stage_d<R, 0>(x, W, tb0, c); break;
-        case 1: if constexpr (R > 2) fwd_stage_d<R, 1>(x, W, tb0, c); break;
-        case 2: if constexpr (R > 4) fwd_stage_d<R, 2>(x, W, tb0, c); break;
-        default: if constexpr (R > 8) fwd_stage_d<R, 3>(x, W, tb0, c); break;
+        case 0: fwd_stage_d<R, 0, SM>(x, W, tb0, c); break;
+        case 1: if constexpr (R > 2) fwd_stage_d<R, 1, SM>(x, W, tb0, c); break;
+        case 2: if constexpr (R > 4) fwd_stage_d<R, 2, SM>(x, W, tb0, c); break;
+        default: if constexpr (R > 8) fwd_stage_d<R, 3, SM>(x, W, tb0, c); break;
     }
 }
-template <int R>
+template <int R, bool SM = false>
 __device__ __forceinline__ void inv_stage_dh(int h, double (&x)[R], const double* W, int tb0, const DblC& c) {
     switch (h) {
-        case 0: inv_stage_d<R, 0>(x, W, tb0, c); break;
-        case 1: if constexpr (R > 2) inv_stage_d<R, 1>(x, W, tb0, c); break;
-        case 2: if constexpr (R > 4) inv_stage_d<R, 2>(x, W, tb0, c); break;
-        default: if constexpr (R > 8) inv_stage_d<R, 3>(x, W, tb0, c); break;
+        case 0: inv_stage_d<R, 0, SM>(x, W, tb0, c); break;
+        case 1: if constexpr (R > 2) inv_stage_d<R, 1, SM>(x, W, tb0, c); break;
+        case 2: if constexpr (R > 4) inv_stage_d<R, 2, SM>(x, W, tb0, c); break;
+        default: if constexpr (R > 8) inv_stage_d<R, 3, SM>(x, W, tb0, c); break;
     }
 }
 template <int R>
@@ -299,14 +335,26 @@ constexpr u64 NTT_DBL_BOUND = 1ull << 41;
 __device__ __forceinline__ int swz128(int e) {  // word index -> swizzled word index
     return (e & ~15) | (((((e >> 1) ^ (e >> 4)) & 7) << 1)) | (e & 1);
 }
-template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, bool DBL, class Ld, class St, bool PRE = false>
+template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, bool DBL, class Ld, class St, bool PRE = false,
+          bool TWSM = false>
 __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
-                                         const NttPassArgs& a, u64* sm, const int bx, const int li, const int z) {
+                                         const NttPassArgs& a, u64* sm, const int bx, const int li, const int z,
+                                         const double* tws = nullptr) {
     using S = NttShape<LOG_T, LOG_R>;
     constexpr int T = S::T, R = S::R, NG = S::NG;
     constexpr int TPS = T / R;  // threads per sub-transform
     constexpr int SROW = IS_COL ? (COLS + 1) : (T + T / 16);
     using V = typename std::conditional<DBL, double, u64>::type;
+    // Row passes whose sub-transform is held by at most one warp's threads
+    // (TPS <= 32): a warp owns 32 / TPS whole rows, stages them itself and
+    // exchanges only with its own lanes, so every synchronisation of the pass
+    // is a __syncwarp — warps never wait for one another (kRowWarpSync).
+    constexpr bool WS = kRowWarpSync && !IS_COL && !PRE && TPS <= 32 && (T * COLS / R) % 32 == 0;
+    constexpr int WWORDS = WS ? (32 / TPS) * T : 1;  // contiguous words a warp owns
+    auto sync_tile = [&]() {
+        if constexpr (WS) __syncwarp();
+        else __syncthreads();
+    };
 
     const int prime = map.prime[li];
     const u64 q = tb.q[prime];
@@ -318,6 +366,11 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
     const double* WD = (INV ? tb.itwd : tb.twd) + (size_t)prime * n;
 
     const int tid = threadIdx.x;
+    // column passes of fp64 limbs: the pass's 2^LOG_T - 1 twiddles (the same for
+    // every column) are staged in shared memory by the kernel, so the
+    // per-stage twiddle reads are LDS instead of LDG queued behind the data
+    // loads and stores (kColTwSmem)
+    if constexpr (TWSM) WD = tws;
     int cc, s;
     if (IS_COL) { cc = tid % COLS; s = tid / COLS; }
     else { s = tid % TPS; cc = tid / TPS; }
@@ -347,19 +400,31 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
     }
     auto loff = [&](int k) -> int { return IS_COL ? (k << S2) : k; };
     auto LD = [&](int k) -> u64 {
+#if HELR_NTT_EXP & 4
+        return (u64)(k * 3 + tid);
+#endif
         if constexpr (LP) return lin[loff(k)];
         else return ld(z, li, prime, goff(k));
     };
     auto LD2 = [&](int k) -> ulonglong2 {
+#if HELR_NTT_EXP & 4
+        return make_ulonglong2(k * 3 + tid, k * 5 + tid);
+#endif
         if constexpr (LP) return *reinterpret_cast<const ulonglong2*>(lin + loff(k));
         else if constexpr (has_vec<Ld>::value) return ld.load2(z, li, prime, goff(k));
         else return make_ulonglong2(0, 0);  // not reached: vector paths need kVec
     };
     auto ST = [&](int k, u64 v) {
+#if HELR_NTT_EXP & 8
+        if (v != 0xDEADBEEFDEADBEEFull) return;
+#endif
         if constexpr (SP) lout[loff(k)] = v;
         else st(z, li, prime, goff(k), v);
     };
     auto ST2 = [&](int k, ulonglong2 v) {
+#if HELR_NTT_EXP & 8
+        if (v.x != 0xDEADBEEFDEADBEEFull) return;
+#endif
         if constexpr (SP) *reinterpret_cast<ulonglong2*>(lout + loff(k)) = v;
         else if constexpr (has_vec<St>::value) st.store2(z, li, prime, goff(k), v);
     };
@@ -410,19 +475,26 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                     // through shared memory (each thread then takes R in a row)
                     constexpr int TOT = T * COLS;
                     const int nthr = T * COLS / R;
+                    const int e0 = WS ? (tid >> 5) * WWORDS + 2 * (tid & 31) : 2 * tid;
+                    const int e1 = WS ? ((tid >> 5) + 1) * WWORDS : TOT;
+                    const int es = WS ? 64 : 2 * nthr;
 #pragma unroll 4
-                    for (int e = 2 * tid; e < TOT; e += 2 * nthr) {
+                    for (int e = e0; e < e1; e += es) {
                         const int c2 = e >> LOG_T, k = e & (T - 1);
                         ulonglong2 v;
+#if HELR_NTT_EXP & 4
+                        v = make_ulonglong2(e * 3 + tid, e * 5 + tid);
+#else
                         if constexpr (LP) v = *reinterpret_cast<const ulonglong2*>(lcta + e);
                         else v = ld.load2(z, li, prime, ((bx * COLS + c2) << LOG_T) + k);
+#endif
                         sm[c2 * SROW + k + (k >> 4)] = v.x;
                         sm[c2 * SROW + k + 1 + ((k + 1) >> 4)] = v.y;
                     }
-                    __syncthreads();
+                    sync_tile();
 #pragma unroll
                     for (int i = 0; i < R; i++) x[i] = in_v(sm[sidx(base + i)]);
-                    __syncthreads();
+                    sync_tile();
                 } else {
 #pragma unroll
                     for (int i = 0; i < R; i++) x[i] = in_v(LD(base + (i << lo)));
@@ -446,19 +518,23 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
         } else {
 #pragma unroll
             for (int i = 0; i < R; i++) x[i] = from_sm(sm[sidx(base + (i << lo))]);
-            if (NG > 2) __syncthreads();
+            if (NG > 2) sync_tile();
         }
+#if HELR_NTT_EXP & 2
+        if (false) {
+#else
         if (!INV) {
+#endif
             const int qhi = LOG_T - g * LOG_R - 1;
             const int qlo = qhi - LOG_R + 1 > 0 ? qhi - LOG_R + 1 : 0;
 #pragma unroll
             for (int qb = qhi; qb >= qlo; qb--) {
                 const int ls = LOG_T - 1 - qb;
                 const int t0 = (wrow << ls) + (base >> (qb + 1));
-                if constexpr (DBL) fwd_stage_dh<R>(qb - lo, x, WD, t0, dc);
+                if constexpr (DBL) fwd_stage_dh<R, TWSM>(qb - lo, x, WD, t0, dc);
                 else fwd_stage_h<R>(qb - lo, x, W2, t0, q, q2);
             }
-        } else {
+        } else if (!(HELR_NTT_EXP & 2)) {
             const int qlo = g * LOG_R;
             const int qhi = (g + 1) * LOG_R < LOG_T ? (g + 1) * LOG_R - 1 : LOG_T - 1;
 #pragma unroll
@@ -470,7 +546,7 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                                        tb.itw1n_sh[prime], q, q2);
                 } else {
                     const int t0 = (wrow << ls) + (base >> (qb + 1));
-                    if constexpr (DBL) inv_stage_dh<R>(qb - lo, x, WD, t0, dc);
+                    if constexpr (DBL) inv_stage_dh<R, TWSM>(qb - lo, x, WD, t0, dc);
                     else inv_stage_h<R>(qb - lo, x, W2, t0, q, q2);
                 }
             }
@@ -504,16 +580,22 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
 #pragma unroll
                     for (int i = 0; i < R; i++) ST(base + (i << lo), y[i]);
                 } else {
-                if (NG > 1) __syncthreads();  // this group's shared-memory reads are done
+                if (NG > 1) sync_tile();  // this group's shared-memory reads are done
 #pragma unroll
                 for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = y[i];
-                __syncthreads();
+                sync_tile();
                 constexpr int TOT = T * COLS;
                 const int nthr = T * COLS / R;
+                const int e0 = WS ? (tid >> 5) * WWORDS + 2 * (tid & 31) : 2 * tid;
+                const int e1 = WS ? ((tid >> 5) + 1) * WWORDS : TOT;
+                const int es = WS ? 64 : 2 * nthr;
 #pragma unroll (kNttEpiUnroll)
-                for (int e = 2 * tid; e < TOT; e += 2 * nthr) {
+                for (int e = e0; e < e1; e += es) {
                     const int c2 = e >> LOG_T, k = e & (T - 1);
                     const u64 v0 = sm[c2 * SROW + k + (k >> 4)], v1 = sm[c2 * SROW + k + 1 + ((k + 1) >> 4)];
+#if HELR_NTT_EXP & 8
+                    if (v0 != 0xDEADBEEFDEADBEEFull) continue;
+#endif
                     if constexpr (SP) *reinterpret_cast<ulonglong2*>(scta + e) = make_ulonglong2(v0, v1);
                     else st.store2(z, li, prime, ((bx * COLS + c2) << LOG_T) + k, make_ulonglong2(v0, v1));
                 }
@@ -536,7 +618,7 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
             }
 #pragma unroll
             for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = to_sm(x[i]);
-            __syncthreads();
+            sync_tile();
         }
     }
 }
@@ -555,6 +637,12 @@ template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, class L
 #ifndef HELR_NTT_MINB512
 #define HELR_NTT_MINB512 3  // 512-thread CTAs (radix-8 register groups, HELR_NTT_LOGR=3)
 #endif
+#ifndef HELR_NTT_COLTW_SMEM
+#define HELR_NTT_COLTW_SMEM 1
+#endif
+#ifndef HELR_NTT_STAGGER
+#define HELR_NTT_STAGGER 0  // ns: delay a hashed half of the first wave's CTAs (phase-stagger experiment)
+#endif
 __global__ void __launch_bounds__((1 << LOG_T) * COLS / (1 << LOG_R),
                                   ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 512 ? HELR_NTT_MINB512 :
                                   ((1 << LOG_T) * COLS / (1 << LOG_R)) >= 256 ? HELR_NTT_MINB : 1)
@@ -566,9 +654,33 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     // the slowest index, so the slower integer-path limb (q_0, listed first)
     // is scheduled in the first waves rather than in the tail
     const int li = NTT_LIMB_MAJOR ? blockIdx.z : blockIdx.y, z = NTT_LIMB_MAJOR ? blockIdx.y : blockIdx.z;
-    if (tb.q[map.prime[li]] < NTT_DBL_BOUND)
-        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true>(ld, st, tb, map, a, sm, blockIdx.x, li, z);
-    else
+#if HELR_NTT_STAGGER
+    {
+        const unsigned lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        if (gridDim.x * gridDim.y * gridDim.z >= 1184 && lin < 592 && ((lin * 2654435761u) >> 31)) {
+            unsigned long long t0, t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            do {
+                __nanosleep(100);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            } while (t1 - t0 < HELR_NTT_STAGGER);
+        }
+    }
+#endif
+    constexpr bool TWS = kColTwSmem && IS_COL && LOG_T >= 6 && ((1 << LOG_T) <= (1 << LOG_T) * COLS / (1 << LOG_R));
+    __shared__ __align__(16) double tws[TWS ? T : 1];
+    if (tb.q[map.prime[li]] < NTT_DBL_BOUND) {
+        const double* twp = nullptr;
+        if constexpr (TWS) {
+            // one coalesced read of the limb's column-pass table per CTA
+            const int prime = map.prime[li];
+            if (threadIdx.x < T)
+                tws[threadIdx.x] = __ldg((INV ? tb.itwd : tb.twd) + ((size_t)prime << a.log_n) + threadIdx.x);
+            __syncthreads();
+            twp = tws;
+        }
+        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true, Ld, St, false, TWS>(ld, st, tb, map, a, sm, blockIdx.x, li, z, twp);
+    } else
         ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, false>(ld, st, tb, map, a, sm, blockIdx.x, li, z);
 }
 

@@ -61,6 +61,7 @@ ntt_pass_tma(const __grid_constant__ CUtensorMap tmap, Geom g, LdBuf ld, St st, 
     extern __shared__ unsigned char ntma_raw[];
     u64* buf = reinterpret_cast<u64*>((reinterpret_cast<uintptr_t>(ntma_raw) + 1023) & ~(uintptr_t)1023);
     u64* bars = buf + 2 * BUF_WORDS;
+    __shared__ __align__(16) double tws[IS_COL ? (1 << LOG_T) : 1];
     const int tid = threadIdx.x;
     if (tid == 0) {
         mbar_init(bars + 0, 1);
@@ -87,11 +88,19 @@ ntt_pass_tma(const __grid_constant__ CUtensorMap tmap, Geom g, LdBuf ld, St st, 
         if (tid == 0 && t + G < g.total) issue(t + G, b ^ 1);  // its buffer was released by the previous tile's closing barrier
         const int bx = t % TILES_PER_LIMB, lz = t / TILES_PER_LIMB;
         const int li = lz / g.count, z = lz - li * g.count;
-        mbar_wait(bars + b, (it >> 1) & 1);
-        u64* sm = buf + b * BUF_WORDS;
         constexpr int S2 = IS_COL ? LOG_N - LOG_T : 0;
-        if (tb.q[map.prime[li]] < NTT_DBL_BOUND)
-            ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true, LdBuf, St, true>(ld, st, tb, map, a, sm, bx, li, z);
+        constexpr bool TWS = kColTwSmem && IS_COL;
+        const bool dbl = tb.q[map.prime[li]] < NTT_DBL_BOUND;
+        if constexpr (TWS) {
+            // the limb's 255 column-pass twiddles into shared memory (the
+            // previous tile's closing barrier released the table)
+            if (dbl) tws[tid] = __ldg((INV ? tb.itwd : tb.twd) + ((size_t)map.prime[li] << LOG_N) + tid);
+        }
+        mbar_wait(bars + b, (it >> 1) & 1);
+        if constexpr (TWS) __syncthreads();
+        u64* sm = buf + b * BUF_WORDS;
+        if (dbl)
+            ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true, LdBuf, St, true, TWS>(ld, st, tb, map, a, sm, bx, li, z, tws);
         else
             ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, false, LdBuf, St, true>(ld, st, tb, map, a, sm, bx, li, z);
         // generic-proxy accesses of this buffer are ordered before the bulk
@@ -130,13 +139,14 @@ inline int sm_count() {
 // HELR_NTT_TMA=1 turns the path on.  Default off: measured slower than the
 // plain passes (0.60 vs 0.50 us per fp64 limb at 112 limbs) —
 // ncu shows the passes wait on the per-stage twiddle loads, not on the tile.
-inline bool enabled() {
+inline int mode() {  // 1: both passes, 2: column passes only, 3: row passes only
     static int on = [] {
         const char* v = getenv("HELR_NTT_TMA");
         return v ? atoi(v) : 0;
     }();
-    return on != 0;
+    return on;
 }
+inline bool enabled() { return mode() != 0; }
 // launches with fewer tiles keep the quarter-size plain tiles
 // (HELR_NTT_TMA_MIN_TILES overrides, e.g. 1 in the parity tests)
 inline long long min_tiles() {
@@ -164,6 +174,7 @@ inline bool usable(int log_n, const LdBuf& ld, const LimbMap& map, int count) {
 template <bool IS_COL, bool INV, class St>
 static bool launch(const LdBuf& ld, const St& st, const Tables& tb, const LimbMap& map, const NttPassArgs& a, int count,
                    cudaStream_t s) {
+    if ((mode() == 2 && !IS_COL) || (mode() == 3 && IS_COL)) return false;
     const long long ext = extent_words(ld, map, count);
     CUtensorMap tm;
     cuuint64_t dims[2], strides[1];
