@@ -147,6 +147,8 @@ struct StCombine {
     const u64* w;
     const u64* wsh;
     const u64* q;
+    const double* qd;     // q and 1/q as doubles (primes below 2^41: lazy sigma sums)
+    const double* qinvd;
     const u64* add_a;
     long long a_is, a_ps;
     const u64* add_p;
@@ -189,11 +191,25 @@ struct StCombine {
             // onto the aligned pair (s, s ^ 1): one index and one 16-byte load per step
             const u64* pp = add_p + (size_t)item * p_is + (size_t)p * n;
             const unsigned eo = 2u * (unsigned)brv_dev(off, log_n) + 1u;
-            for (int t = 0; t < ngal; t++) {
-                const int src = galois_perm_e(eo, (u64)gal[t], log_n);
-                const ulonglong2 pr = ld2(pp + (src & ~1));
-                r0 = add_mod(r0, (src & 1) ? pr.y : pr.x, qq);
-                r1 = add_mod(r1, (src & 1) ? pr.x : pr.y, qq);
+            if (qq < NTT_DBL_BOUND) {
+                // primes below 2^41: plain 64-bit sums of the <= 2^11 gathered
+                // residues (< 2^52), one exact fp64 reduction at the end
+                for (int t = 0; t < ngal; t++) {
+                    const int src = galois_perm_e(eo, (u64)gal[t], log_n);
+                    const ulonglong2 pr = ld2(pp + (src & ~1));
+                    r0 += (src & 1) ? pr.y : pr.x;
+                    r1 += (src & 1) ? pr.x : pr.y;
+                }
+                const DblC dc{qd[p], qinvd[p]};
+                r0 = d2u_canon(u2d(r0), dc);
+                r1 = d2u_canon(u2d(r1), dc);
+            } else {
+                for (int t = 0; t < ngal; t++) {
+                    const int src = galois_perm_e(eo, (u64)gal[t], log_n);
+                    const ulonglong2 pr = ld2(pp + (src & ~1));
+                    r0 = add_mod(r0, (src & 1) ? pr.y : pr.x, qq);
+                    r1 = add_mod(r1, (src & 1) ? pr.x : pr.y, qq);
+                }
             }
         }
         st2(out + (size_t)item * out_is + (size_t)poly * out_ps + (size_t)p * n + off, r0, r1);
@@ -212,7 +228,7 @@ static inline StCombine st_combine(const helr_ctx* c, u64* out, long long out_is
     StCombine f;
     f.out = out; f.out_is = out_is; f.out_ps = out_ps;
     f.x = x; f.x_is = x_is; f.x_ps = x_ps;
-    f.w = w; f.wsh = wsh; f.q = c->t.q;
+    f.w = w; f.wsh = wsh; f.q = c->t.q; f.qd = c->t.qd; f.qinvd = c->t.qinvd;
     f.add_a = nullptr; f.a_is = f.a_ps = 0;
     f.add_p = nullptr; f.p_is = 0;
     f.ngal = 0; f.log_n = c->log_n; f.n = c->n; f.per_poly = per_poly;

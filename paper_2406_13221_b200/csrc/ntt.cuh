@@ -189,15 +189,20 @@ __device__ __forceinline__ double reduce_d(double x, const DblC& c) {
 __device__ __forceinline__ double u2d(u64 x) {  // x < 2^52
     return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), NTT_TWO52);
 }
+// r < 0 ? r + q : r with the sign test on the integer pipe (an exact zero
+// difference is +0 in round-to-nearest, so the sign bit alone decides): the
+// fp64 pipe, which bounds these kernels, is spared the DSETP
+__device__ __forceinline__ double wrap_neg(double r, double q) {
+    const double rq = __dadd_rn(r, q);
+    return __double2hiint(r) < 0 ? rq : r;
+}
 __device__ __forceinline__ u64 d2u_canon(double x, const DblC& c) {  // integer-valued |x| < 2^50 -> [0, q)
-    double r = reduce_d(x, c);
-    r = r < 0.0 ? __dadd_rn(r, c.q) : r;
+    const double r = wrap_neg(reduce_d(x, c), c.q);
     return (u64)__double_as_longlong(__dadd_rn(r, NTT_TWO52)) & 0x000FFFFFFFFFFFFFull;
 }
 // integer-valued |x| < 2^50 -> its residue in [0, q) as a double
 __device__ __forceinline__ double d2d_canon(double x, const DblC& c) {
-    const double r = reduce_d(x, c);
-    return r < 0.0 ? __dadd_rn(r, c.q) : r;
+    return wrap_neg(reduce_d(x, c), c.q);
 }
 // A stage's R / 2^(H+1) twiddles are contiguous and, when there are two or
 // more, start at an even index (the low bits of the register group's base
