@@ -437,8 +437,11 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
         return IS_COL ? (k * SROW + cc) : (cc * SROW + k + (k >> 4));
     };
     const bool raw_in = DBL && a.raw_in;
+    // fp64 limbs: loads only reinterpret; canonical u64 inputs are converted in
+    // one block after the group-0 load (a single uniform branch per pass
+    // instead of a select per element)
     auto in_v = [&](u64 v) -> V {
-        if constexpr (DBL) return raw_in ? __longlong_as_double((long long)v) : u2d(v);
+        if constexpr (DBL) return __longlong_as_double((long long)v);
         else return v;
     };
     auto to_sm = [&](V v) -> u64 {
@@ -479,12 +482,15 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                     // coalesced prologue: the CTA's T * COLS contiguous inputs
                     // through shared memory (each thread then takes R in a row)
                     constexpr int TOT = T * COLS;
-                    const int nthr = T * COLS / R;
+                    constexpr int nthr = T * COLS / R;
+                    // constant trip count: every thread moves TOT / (2 nthr) pairs
                     const int e0 = WS ? (tid >> 5) * WWORDS + 2 * (tid & 31) : 2 * tid;
-                    const int e1 = WS ? ((tid >> 5) + 1) * WWORDS : TOT;
-                    const int es = WS ? 64 : 2 * nthr;
+                    constexpr int es = WS ? 64 : 2 * nthr;
+                    constexpr int NIT = WS ? WWORDS / 64 : TOT / (2 * nthr);
+                    static_assert(NIT * es == (WS ? WWORDS : TOT), "staging loop must tile the CTA's words");
 #pragma unroll 4
-                    for (int e = e0; e < e1; e += es) {
+                    for (int u = 0; u < NIT; u++) {
+                        const int e = e0 + u * es;
                         const int c2 = e >> LOG_T, k = e & (T - 1);
                         ulonglong2 v;
 #if HELR_NTT_EXP & 4
@@ -519,6 +525,12 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
             } else {
 #pragma unroll
                 for (int i = 0; i < R; i++) x[i] = in_v(LD(base + (i << lo)));
+            }
+            if constexpr (DBL) {
+                if (!raw_in) {
+#pragma unroll
+                    for (int i = 0; i < R; i++) x[i] = u2d((u64)__double_as_longlong(x[i]));
+                }
             }
         } else {
 #pragma unroll
@@ -558,16 +570,21 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
         }
         if (g == NG - 1) {
             u64 y[R];
+            if constexpr (DBL) {
+                // one uniform branch per pass, then straight-line conversions
+                if (a.raw_out) {  // forward: |x| < 10 q; inverse: reduce the 2^8 growth
 #pragma unroll
-            for (int i = 0; i < R; i++) {
-                if constexpr (DBL) {
-                    if (a.raw_out)  // forward: |x| < 10 q; inverse: reduce the 2^8 growth
-                        y[i] = (u64)__double_as_longlong(INV ? reduce_d(x[i], dc) : x[i]);
-                    else if (a.dbl_out)
-                        y[i] = (u64)__double_as_longlong(d2d_canon(x[i], dc));
-                    else
-                        y[i] = d2u_canon(x[i], dc);  // canonical [0, q)
+                    for (int i = 0; i < R; i++) y[i] = (u64)__double_as_longlong(INV ? reduce_d(x[i], dc) : x[i]);
+                } else if (a.dbl_out) {
+#pragma unroll
+                    for (int i = 0; i < R; i++) y[i] = (u64)__double_as_longlong(d2d_canon(x[i], dc));
                 } else {
+#pragma unroll
+                    for (int i = 0; i < R; i++) y[i] = d2u_canon(x[i], dc);  // canonical [0, q)
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < R; i++) {
                     u64 v = x[i];
                     if (a.final_out) {  // forward [0, 8q), inverse [0, 4q) -> [0, q)
                         if (!INV) v = v >= q2 ? v - q2 : v;
@@ -590,12 +607,14 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                 for (int i = 0; i < R; i++) sm[sidx(base + (i << lo))] = y[i];
                 sync_tile();
                 constexpr int TOT = T * COLS;
-                const int nthr = T * COLS / R;
+                constexpr int nthr = T * COLS / R;
                 const int e0 = WS ? (tid >> 5) * WWORDS + 2 * (tid & 31) : 2 * tid;
-                const int e1 = WS ? ((tid >> 5) + 1) * WWORDS : TOT;
-                const int es = WS ? 64 : 2 * nthr;
+                constexpr int es = WS ? 64 : 2 * nthr;
+                constexpr int NIT = WS ? WWORDS / 64 : TOT / (2 * nthr);
+                static_assert(NIT * es == (WS ? WWORDS : TOT), "staging loop must tile the CTA's words");
 #pragma unroll (kNttEpiUnroll)
-                for (int e = e0; e < e1; e += es) {
+                for (int u = 0; u < NIT; u++) {
+                    const int e = e0 + u * es;
                     const int c2 = e >> LOG_T, k = e & (T - 1);
                     const u64 v0 = sm[c2 * SROW + k + (k >> 4)], v1 = sm[c2 * SROW + k + 1 + ((k + 1) >> 4)];
 #if HELR_NTT_EXP & 8
