@@ -140,6 +140,23 @@ __device__ __forceinline__ u128acc dresolve(const dacc& a) {  // hh 2^42 + mid 2
 struct StCombine {
     static constexpr bool kVec = true;
     static constexpr bool kTile = true;
+    // fp64 limbs hand the storer the pass's raw doubles (integer-valued, any
+    // representative, |v| < 2^46): the combine runs on the fp64 pipe — one
+    // exact twiddle-style product and ONE canonicalisation for the whole
+    // (x - v) w + addend + sigma-sum — instead of canonicalising v and then
+    // doing a 64-bit integer Shoup product
+    static constexpr bool kRawD = true;
+    // per-thread context of one (item, limb): decoded once per pass, not per pair
+    struct Ctx {
+        const u64* xb;
+        const u64* ab;
+        const u64* pb;
+        u64* ob;
+        u64 qq, wp, wps;
+        double wd;
+        DblC dc;
+        bool dbl;
+    };
     u64* out;
     long long out_is, out_ps;
     const u64* x;
@@ -175,6 +192,86 @@ struct StCombine {
         u64 r = shoup(sub_mod(xv, v, qq), w[p], wsh[p], qq);
         const u64 av = add_a ? add_a[(size_t)item * a_is + (size_t)poly * a_ps + (size_t)p * n + off] : 0;
         out[(size_t)item * out_is + (size_t)poly * out_ps + (size_t)p * n + off] = addends(r, item, poly, p, off, qq, av);
+    }
+    __device__ __forceinline__ Ctx prep(int z, int li) const {
+        int item, poly, p;
+        decode(z, li, item, poly, p);
+        Ctx c;
+        c.qq = q[p]; c.wp = w[p]; c.wps = wsh[p];
+        c.dbl = c.qq < NTT_DBL_BOUND;
+        c.dc = DblC{qd[p], qinvd[p]};
+        c.wd = u2d(c.wp & 0x000FFFFFFFFFFFFFull);  // used only when dbl (w < q < 2^41)
+        c.xb = x + (size_t)item * x_is + (size_t)poly * x_ps + (size_t)p * n;
+        c.ab = add_a ? add_a + (size_t)item * a_is + (size_t)poly * a_ps + (size_t)p * n : nullptr;
+        c.pb = (add_p && poly == 0) ? add_p + (size_t)item * p_is + (size_t)p * n : nullptr;
+        c.ob = out + (size_t)item * out_is + (size_t)poly * out_ps + (size_t)p * n;
+        return c;
+    }
+    // v: fp64 limbs -> raw double bits (kRawD), integer limbs -> canonical u64
+    __device__ __forceinline__ void store2c(const Ctx& c, int off, ulonglong2 v) const {
+        const ulonglong2 xv = ld2(c.xb + off);
+        if (c.dbl) {
+            double r0 = mulmod_d(__dsub_rn(u2d(xv.x), __longlong_as_double((long long)v.x)), c.wd, c.dc);
+            double r1 = mulmod_d(__dsub_rn(u2d(xv.y), __longlong_as_double((long long)v.y)), c.wd, c.dc);
+            if (c.ab) {
+                const ulonglong2 av = ld2(c.ab + off);
+                r0 = __dadd_rn(r0, u2d(av.x));
+                r1 = __dadd_rn(r1, u2d(av.y));
+            }
+            if (c.pb) {
+                // plain 64-bit sums of the <= 2^11 gathered residues (< 2^52), added as exact doubles
+                const unsigned eo = 2u * (unsigned)brv_dev(off, log_n) + 1u;
+                u64 s0 = 0, s1 = 0;
+                for (int t = 0; t < ngal; t++) {
+                    const int src = galois_perm_e(eo, (u64)gal[t], log_n);
+                    const ulonglong2 pr = ld2(c.pb + (src & ~1));
+                    s0 += (src & 1) ? pr.y : pr.x;
+                    s1 += (src & 1) ? pr.x : pr.y;
+                }
+                r0 = __dadd_rn(r0, u2d(s0));
+                r1 = __dadd_rn(r1, u2d(s1));
+            }
+            st2(c.ob + off, d2u_canon(r0, c.dc), d2u_canon(r1, c.dc));
+            return;
+        }
+        const u64 qq = c.qq;
+        u64 r0 = shoup(sub_mod(xv.x, v.x, qq), c.wp, c.wps, qq);
+        u64 r1 = shoup(sub_mod(xv.y, v.y, qq), c.wp, c.wps, qq);
+        if (c.ab) {
+            const ulonglong2 av = ld2(c.ab + off);
+            r0 = add_mod(r0, av.x, qq);
+            r1 = add_mod(r1, av.y, qq);
+        }
+        if (c.pb) {
+            const unsigned eo = 2u * (unsigned)brv_dev(off, log_n) + 1u;
+            for (int t = 0; t < ngal; t++) {
+                const int src = galois_perm_e(eo, (u64)gal[t], log_n);
+                const ulonglong2 pr = ld2(c.pb + (src & ~1));
+                r0 = add_mod(r0, (src & 1) ? pr.y : pr.x, qq);
+                r1 = add_mod(r1, (src & 1) ? pr.x : pr.y, qq);
+            }
+        }
+        st2(c.ob + off, r0, r1);
+    }
+    // single element (passes whose last register group is strided)
+    __device__ __forceinline__ void store1c(const Ctx& c, int off, u64 v) const {
+        const u64 xv = c.xb[off];
+        if (c.dbl) {
+            double r = mulmod_d(__dsub_rn(u2d(xv), __longlong_as_double((long long)v)), c.wd, c.dc);
+            if (c.ab) r = __dadd_rn(r, u2d(c.ab[off]));
+            if (c.pb) {
+                u64 s0 = 0;
+                for (int t = 0; t < ngal; t++) s0 += c.pb[galois_perm(off, (u64)gal[t], log_n)];
+                r = __dadd_rn(r, u2d(s0));
+            }
+            c.ob[off] = d2u_canon(r, c.dc);
+            return;
+        }
+        u64 r = shoup(sub_mod(xv, v, c.qq), c.wp, c.wps, c.qq);
+        if (c.ab) r = add_mod(r, c.ab[off], c.qq);
+        if (c.pb)
+            for (int t = 0; t < ngal; t++) r = add_mod(r, c.pb[galois_perm(off, (u64)gal[t], log_n)], c.qq);
+        c.ob[off] = r;
     }
     __device__ __forceinline__ void store2(int z, int li, int, int off, ulonglong2 v) const {
         int item, poly, p;

@@ -319,6 +319,18 @@ __device__ __forceinline__ void inv_last_dh(int h, double (&x)[R], double ni, do
     }
 }
 
+// Storers with kRawD take fp64 limbs' outputs as raw double bits and a
+// per-thread context (prep / store2c / store1c): see StCombine (ks.cuh).
+template <class F, class = void>
+struct has_rawd { static constexpr bool value = false; };
+template <class F>
+struct has_rawd<F, decltype((void)F::kRawD)> { static constexpr bool value = F::kRawD; };
+
+template <class F, bool = has_rawd<F>::value>
+struct storer_ctx { struct type {}; };
+template <class F>
+struct storer_ctx<F, true> { using type = typename F::Ctx; };
+
 // Loaders / storers with kPtr expose the base address of limb li of item z
 // (plain strided buffers): the pass then addresses its elements as one
 // pointer plus compile-time offsets instead of a 64-bit product per element.
@@ -419,11 +431,13 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
         else if constexpr (has_vec<Ld>::value) return ld.load2(z, li, prime, goff(k));
         else return make_ulonglong2(0, 0);  // not reached: vector paths need kVec
     };
+    typename storer_ctx<St>::type sctx;  // filled right before the stores (keeps it out of the butterflies' registers)
     auto ST = [&](int k, u64 v) {
 #if HELR_NTT_EXP & 8
         if (v != 0xDEADBEEFDEADBEEFull) return;
 #endif
         if constexpr (SP) lout[loff(k)] = v;
+        else if constexpr (has_rawd<St>::value) st.store1c(sctx, goff(k), v);
         else st(z, li, prime, goff(k), v);
     };
     auto ST2 = [&](int k, ulonglong2 v) {
@@ -431,6 +445,7 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
         if (v.x != 0xDEADBEEFDEADBEEFull) return;
 #endif
         if constexpr (SP) *reinterpret_cast<ulonglong2*>(lout + loff(k)) = v;
+        else if constexpr (has_rawd<St>::value) st.store2c(sctx, goff(k), v);
         else if constexpr (has_vec<St>::value) st.store2(z, li, prime, goff(k), v);
     };
     auto sidx = [&](int k) -> int {
@@ -570,7 +585,12 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
         }
         if (g == NG - 1) {
             u64 y[R];
-            if constexpr (DBL) {
+            constexpr bool RAWD = has_rawd<St>::value;
+            if constexpr (RAWD) sctx = st.prep(z, li);
+            if constexpr (DBL && RAWD) {
+#pragma unroll
+                for (int i = 0; i < R; i++) y[i] = (u64)__double_as_longlong(x[i]);  // the storer reduces
+            } else if constexpr (DBL) {
                 // one uniform branch per pass, then straight-line conversions
                 if (a.raw_out) {  // forward: |x| < 10 q; inverse: reduce the 2^8 growth
 #pragma unroll
@@ -621,6 +641,8 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
                     if (v0 != 0xDEADBEEFDEADBEEFull) continue;
 #endif
                     if constexpr (SP) *reinterpret_cast<ulonglong2*>(scta + e) = make_ulonglong2(v0, v1);
+                    else if constexpr (has_rawd<St>::value)
+                        st.store2c(sctx, ((bx * COLS + c2) << LOG_T) + k, make_ulonglong2(v0, v1));
                     else st.store2(z, li, prime, ((bx * COLS + c2) << LOG_T) + k, make_ulonglong2(v0, v1));
                 }
                 }
