@@ -21,7 +21,7 @@ static inline bool specials_fp64(const helr_ctx* c) {
 // Centred conversion (see oracle oc_moddown_convert): subtract r*P with
 // r = round(sum_k y_k / p_k) evaluated in IEEE double without contraction,
 // so the ModDown error is the zero-mean rounding of x / P.
-template <int MK>
+template <int MK, bool ALLD>
 __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n,
                                int nl, int K, int L, const u64* phinv, const u64* phinv_sh, const u64* phm,
                                const u64* phms, const u64* pinv_dbl, const u64* pm, const u64* pm_sh, Tables tb) {
@@ -31,10 +31,25 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
     const int ne = nl + K;
     const u64* ap = acc + (size_t)b * acc_item_stride + (size_t)poly * ne * n;
     u64* mp = mdc + (size_t)b * mdc_item_stride + (size_t)poly * L * n;
+    // the K x nl target weights as doubles, converted once per CTA (every
+    // thread used to convert each of them): shared-memory broadcast reads
+    __shared__ double wsm[MK <= 8 ? MK * HELR_MAXP : 1];
+    constexpr bool WSM = MK <= 8;
+    if constexpr (WSM) {
+        for (int e = threadIdx.x; e < K * nl; e += blockDim.x) {
+            const int k = e / nl, p = e - k * nl;
+            wsm[k * HELR_MAXP + p] = u2d(phm[(size_t)k * L + p] & 0x000FFFFFFFFFFFFFull);
+        }
+        __syncthreads();
+    }
     const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (i >= n) return;
-    u64 z0[MK], z1[MK];
+    // ALLD (host: every source prime below 2^41): the sources live only as
+    // exact doubles; otherwise integer views are kept as well
+    u64 z0[ALLD ? 1 : MK], z1[ALLD ? 1 : MK];
+    double zd0[MK], zd1[MK];  // sources as exact doubles (special primes below 2^41)
     double v0 = 0.0, v1 = 0.0;
+    bool dsrc = true;
 #pragma unroll
     for (int k = 0; k < MK; k++) {
         if (k < K) {
@@ -42,14 +57,15 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
             const double inv = __longlong_as_double((long long)pinv_dbl[k]);
             const ulonglong2 x = ld2(ap + (size_t)(nl + k) * n + i);
             double d0, d1;  // canonical z as exact doubles (no u64 -> f64 conversions)
-            if (pk < NTT_DBL_BOUND) {
+            if (ALLD || pk < NTT_DBL_BOUND) {
                 const DblC dk{tb.qd[L + k], tb.qinvd[L + k]};
                 const double w = u2d(phinv[k]);
                 d0 = d2d_canon(mulmod_d(u2d(x.x), w, dk), dk);
                 d1 = d2d_canon(mulmod_d(u2d(x.y), w, dk), dk);
-                z0[k] = dexact(d0);
-                z1[k] = dexact(d1);
-            } else {
+                zd0[k] = d0;
+                zd1[k] = d1;
+            } else if constexpr (!ALLD) {
+                dsrc = false;
                 z0[k] = shoup(x.x, phinv[k], phinv_sh[k], pk);
                 z1[k] = shoup(x.y, phinv[k], phinv_sh[k], pk);
                 d0 = __ull2double_rn(z0[k]);
@@ -61,15 +77,14 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
     }
     const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
     const u64 rr1 = (u64)__double2ull_rd(__dadd_rn(v1, 0.5));
-    // sources as exact doubles when every special prime is below 2^41
-    bool dsrc = true;
-    double zd0[MK], zd1[MK];
+    // integer views of the fp64 sources for integer-path targets (ALLD: made at use)
+    if constexpr (!ALLD) {
 #pragma unroll
-    for (int k = 0; k < MK; k++) {
-        if (k < K) {
-            dsrc = dsrc && tb.q[L + k] < NTT_DBL_BOUND;
-            zd0[k] = u2d(z0[k] & 0x000FFFFFFFFFFFFFull);
-            zd1[k] = u2d(z1[k] & 0x000FFFFFFFFFFFFFull);
+        for (int k = 0; k < MK; k++) {
+            if (k < K && tb.q[L + k] < NTT_DBL_BOUND) {
+                z0[k] = dexact(zd0[k]);
+                z1[k] = dexact(zd1[k]);
+            }
         }
     }
     for (int p = 0; p < nl; p++) {
@@ -81,7 +96,7 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
 #pragma unroll
             for (int k = 0; k < MK; k++) {
                 if (k < K) {
-                    const double wd = u2d(phm[(size_t)k * L + p]);
+                    const double wd = WSM ? wsm[k * HELR_MAXP + p] : u2d(phm[(size_t)k * L + p]);
                     s0 = __dadd_rn(s0, mulmod_d(zd0[k], wd, dc));
                     s1 = __dadd_rn(s1, mulmod_d(zd1[k], wd, dc));
                 }
@@ -96,8 +111,9 @@ __global__ void k_moddown_conv(const u64* acc, long long acc_item_stride, u64* m
         for (int k = 0; k < MK; k++) {
             if (k < K) {
                 const u64 w = phm[(size_t)k * L + p], ws = phms[(size_t)k * L + p];
-                s0 = add_mod(s0, shoup(z0[k], w, ws, q), q);
-                s1 = add_mod(s1, shoup(z1[k], w, ws, q), q);
+                const u64 zk0 = ALLD ? dexact(zd0[k]) : z0[ALLD ? 0 : k], zk1 = ALLD ? dexact(zd1[k]) : z1[ALLD ? 0 : k];
+                s0 = add_mod(s0, shoup(zk0, w, ws, q), q);
+                s1 = add_mod(s1, shoup(zk1, w, ws, q), q);
             }
         }
         // canonical residues: with a wide source prime no limb takes the fp64
@@ -164,10 +180,18 @@ int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const KsWs& 
     {
         ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + nl), s);
         // register arrays sized to K (dnum 1 rings have K up to ~31)
-        auto conv = K <= 4 ? k_moddown_conv<4>
-                  : K <= 8 ? k_moddown_conv<8>
-                  : K <= 16 ? k_moddown_conv<16>
-                  : K <= 32 ? k_moddown_conv<32> : k_moddown_conv<HELR_MAXP>;
+        bool alld = true;  // every special prime on the fp64 path
+        for (int k = 0; k < K; k++) alld = alld && c->primes[L + k] < NTT_DBL_BOUND;
+        auto conv = alld ? (K <= 4 ? k_moddown_conv<4, true>
+                            : K == 5 ? k_moddown_conv<5, true>
+                            : K == 6 ? k_moddown_conv<6, true>
+                            : K <= 8 ? k_moddown_conv<8, true>
+                            : K <= 16 ? k_moddown_conv<16, true>
+                            : K <= 32 ? k_moddown_conv<32, true> : k_moddown_conv<HELR_MAXP, true>)
+                         : (K <= 4 ? k_moddown_conv<4, false>
+                            : K <= 8 ? k_moddown_conv<8, false>
+                            : K <= 16 ? k_moddown_conv<16, false>
+                            : K <= 32 ? k_moddown_conv<32, false> : k_moddown_conv<HELR_MAXP, false>);
         launch_pdl(conv, g, dim3(128), 0, s, (const u64*)w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, c->md_phinv,
                    c->md_phinv_sh, c->md_phmod, c->md_phmod_sh, c->md_pinv_dbl, c->pmod, c->pmod_sh, c->t);
         CHECK_KERNEL("ks moddown conv");
@@ -200,7 +224,7 @@ int ks_moddown(helr_ctx* c, int level, const KsEpilogue& ep, int B, const KsWs& 
 // over Q_{l-1}: centred fast conversion from {p_0..p_{K-1}, q_l} (coefficient
 // form) to Q_{l-1}, NTT, then (acc_i - conv_i) * (P q_l)^-1.  Saves the
 // separate rescale's INTT + l NTTs per polynomial.
-template <int MK>
+template <int MK, bool ALLD>
 __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, long long mdc_item_stride, int n, int nl,
                            int K, int L, MrTab mt, Tables tb) {
     pdl_begin();
@@ -209,10 +233,21 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
     const int ne = nl + K, l = nl - 1, ns = K + 1;
     const u64* ap = acc + (size_t)b * acc_item_stride + (size_t)poly * ne * n;
     u64* mp = mdc + (size_t)b * mdc_item_stride + (size_t)poly * L * n;
+    __shared__ double wsm[MK <= 8 ? MK * HELR_MAXP : 1];  // target weights as doubles (see k_moddown_conv)
+    constexpr bool WSM = MK <= 8;
+    if constexpr (WSM) {
+        for (int e = threadIdx.x; e < ns * l; e += blockDim.x) {
+            const int k = e / l, p = e - k * l;
+            wsm[k * HELR_MAXP + p] = u2d(mt.hm[(size_t)k * L + p] & 0x000FFFFFFFFFFFFFull);
+        }
+        __syncthreads();
+    }
     const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (i >= n) return;
-    u64 z0[MK], z1[MK];
+    u64 z0[ALLD ? 1 : MK], z1[ALLD ? 1 : MK];
+    double zd0[MK], zd1[MK];
     double v0 = 0.0, v1 = 0.0;
+    bool dsrc = true;
 #pragma unroll
     for (int k = 0; k < MK; k++) {
         if (k < ns) {
@@ -221,15 +256,16 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
             const double inv = __longlong_as_double((long long)mt.dinv[k]);
             const ulonglong2 x = ld2(ap + (size_t)lim * n + i);
             double d0, d1;  // canonical z as exact doubles (no u64 -> f64 conversions)
-            if (m < NTT_DBL_BOUND) {
+            if (ALLD || m < NTT_DBL_BOUND) {
                 const int pm = k < K ? L + k : l;
                 const DblC dk{tb.qd[pm], tb.qinvd[pm]};
                 const double w = u2d(mt.hv[k]);
                 d0 = d2d_canon(mulmod_d(u2d(x.x), w, dk), dk);
                 d1 = d2d_canon(mulmod_d(u2d(x.y), w, dk), dk);
-                z0[k] = dexact(d0);
-                z1[k] = dexact(d1);
-            } else {
+                zd0[k] = d0;
+                zd1[k] = d1;
+            } else if constexpr (!ALLD) {
+                dsrc = false;
                 z0[k] = shoup(x.x, mt.hv[k], mt.hvs[k], m);
                 z1[k] = shoup(x.y, mt.hv[k], mt.hvs[k], m);
                 d0 = __ull2double_rn(z0[k]);
@@ -241,14 +277,13 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
     }
     const u64 rr0 = (u64)__double2ull_rd(__dadd_rn(v0, 0.5));
     const u64 rr1 = (u64)__double2ull_rd(__dadd_rn(v1, 0.5));
-    bool dsrc = true;
-    double zd0[MK], zd1[MK];
+    if constexpr (!ALLD) {
 #pragma unroll
-    for (int k = 0; k < MK; k++) {
-        if (k < ns) {
-            dsrc = dsrc && tb.q[k < K ? L + k : l] < NTT_DBL_BOUND;
-            zd0[k] = u2d(z0[k] & 0x000FFFFFFFFFFFFFull);
-            zd1[k] = u2d(z1[k] & 0x000FFFFFFFFFFFFFull);
+        for (int k = 0; k < MK; k++) {
+            if (k < ns && tb.q[k < K ? L + k : l] < NTT_DBL_BOUND) {
+                z0[k] = dexact(zd0[k]);
+                z1[k] = dexact(zd1[k]);
+            }
         }
     }
     for (int p = 0; p < l; p++) {
@@ -260,7 +295,7 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
 #pragma unroll
             for (int k = 0; k < MK; k++) {
                 if (k < ns) {
-                    const double wd = u2d(mt.hm[(size_t)k * L + p]);
+                    const double wd = WSM ? wsm[k * HELR_MAXP + p] : u2d(mt.hm[(size_t)k * L + p]);
                     s0 = __dadd_rn(s0, mulmod_d(zd0[k], wd, dc));
                     s1 = __dadd_rn(s1, mulmod_d(zd1[k], wd, dc));
                 }
@@ -274,8 +309,9 @@ __global__ void k_mdr_conv(const u64* acc, long long acc_item_stride, u64* mdc, 
         for (int k = 0; k < MK; k++) {
             if (k < ns) {
                 const u64 w = mt.hm[(size_t)k * L + p], ws = mt.hms[(size_t)k * L + p];
-                s0 = add_mod(s0, shoup(z0[k], w, ws, q), q);
-                s1 = add_mod(s1, shoup(z1[k], w, ws, q), q);
+                const u64 zk0 = ALLD ? dexact(zd0[k]) : z0[ALLD ? 0 : k], zk1 = ALLD ? dexact(zd1[k]) : z1[ALLD ? 0 : k];
+                s0 = add_mod(s0, shoup(zk0, w, ws, q), q);
+                s1 = add_mod(s1, shoup(zk1, w, ws, q), q);
             }
         }
         // canonical residues (see k_moddown_conv)
@@ -328,10 +364,18 @@ int ks_moddown_rescale(helr_ctx* c, int level, u64* out, long long os, int B, co
     {
         dim3 g(blocks_for(n / 2, 128), 2 * B);
         ProfScope ps(PROF_MODDOWN, 8.0 * n * 2.0 * B * (K + 1 + l), s);
-        auto conv = K + 1 <= 4 ? k_mdr_conv<4>
-                  : K + 1 <= 8 ? k_mdr_conv<8>
-                  : K + 1 <= 16 ? k_mdr_conv<16>
-                  : K + 1 <= 32 ? k_mdr_conv<32> : k_mdr_conv<HELR_MAXP>;
+        bool alld = c->primes[l] < NTT_DBL_BOUND;  // every source prime (specials and q_l) on the fp64 path
+        for (int k = 0; k < K; k++) alld = alld && c->primes[L + k] < NTT_DBL_BOUND;
+        auto conv = alld ? (K + 1 <= 4 ? k_mdr_conv<4, true>
+                            : K + 1 == 5 ? k_mdr_conv<5, true>
+                            : K + 1 == 6 ? k_mdr_conv<6, true>
+                            : K + 1 <= 8 ? k_mdr_conv<8, true>
+                            : K + 1 <= 16 ? k_mdr_conv<16, true>
+                            : K + 1 <= 32 ? k_mdr_conv<32, true> : k_mdr_conv<HELR_MAXP, true>)
+                         : (K + 1 <= 4 ? k_mdr_conv<4, false>
+                            : K + 1 <= 8 ? k_mdr_conv<8, false>
+                            : K + 1 <= 16 ? k_mdr_conv<16, false>
+                            : K + 1 <= 32 ? k_mdr_conv<32, false> : k_mdr_conv<HELR_MAXP, false>);
         launch_pdl(conv, g, dim3(128), 0, s, (const u64*)w.acc, w.acc_s, w.mdc, w.mdc_s, n, nl, K, L, mt, c->t);
         CHECK_KERNEL("mdr conv");
     }
