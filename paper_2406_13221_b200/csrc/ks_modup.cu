@@ -40,6 +40,17 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
     u64* ext = a.ext + (size_t)b * a.ext_item_stride + (size_t)j * a.ext_digit_stride;
     const u64* coef = a.coef + (size_t)b * a.coef_stride;
     const u64* d = a.d + (size_t)b * a.d_stride;
+    // the digit's ns x nt target weights as doubles, converted once per CTA
+    // (shared-memory broadcast reads instead of a load + conversion per term)
+    constexpr bool WSM = MA <= 8;
+    __shared__ double wsm[WSM ? MA * HELR_MAXP : 1];
+    if constexpr (WSM) {
+        for (int e = threadIdx.x; e < ns * nt; e += blockDim.x) {
+            const int k = e / nt, t = e - k * nt;
+            wsm[k * HELR_MAXP + t] = u2d(hm[(size_t)k * nt + t] & 0x000FFFFFFFFFFFFFull);
+        }
+        __syncthreads();
+    }
     const int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (i >= a.n) return;
     u64 y0[MA], y1[MA];
@@ -84,12 +95,12 @@ __global__ void k_modup(ModUpArgs a, Tables tb) {
 #pragma unroll
             for (int k = 0; k < MA; k++) {
                 if (k < ns) {
-                    const u64 w = hm[(size_t)k * nt + t];
                     if (ydok[k]) {
-                        const double wd = u2d(w);
+                        const double wd = WSM ? wsm[k * HELR_MAXP + t] : u2d(hm[(size_t)k * nt + t]);
                         s0 = __dadd_rn(s0, mulmod_d(yd0[k], wd, dc));
                         s1 = __dadd_rn(s1, mulmod_d(yd1[k], wd, dc));
                     } else {  // wide source prime (q_0): integer Shoup, result < q
+                        const u64 w = hm[(size_t)k * nt + t];
                         const u64 ws = hms[(size_t)k * nt + t];
                         s0 = __dadd_rn(s0, u2d(shoup(y0[k], w, ws, q)));
                         s1 = __dadd_rn(s1, u2d(shoup(y1[k], w, ws, q)));
