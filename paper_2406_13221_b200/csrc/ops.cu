@@ -38,35 +38,48 @@ __device__ __forceinline__ void ew_decode(long long idx, const EwGeom& g, int& i
 }
 
 
+// one element; op is uniform across the launch
+__device__ __forceinline__ u64 ew_apply(int op, u64 x, u64 bv, int poly, u64 q, int limb, const Tables& tb) {
+    switch (op) {
+        case EW_ADD: return add_mod(x, bv, q);
+        case EW_SUB: return sub_mod(x, bv, q);
+        case EW_ADDC:
+        case EW_ADDPT: return poly == 0 ? add_mod(x, bv, q) : x;
+        case EW_REDUCE: return barrett128(u128v{0, x}, q, tb.br1[limb], tb.br0[limb]);
+        default:
+            if (q < NTT_DBL_BOUND) {
+                const DblC dc{tb.qd[limb], tb.qinvd[limb]};
+                return d2u_canon(mulmod_d(u2d(x), u2d(bv), dc), dc);
+            }
+            return mul_mod(x, bv, q, tb.br1[limb], tb.br0[limb]);
+    }
+}
+// Two consecutive coefficients per thread (16-byte accesses, one index
+// decode per pair); n is even for every ring.
 __global__ void k_elementwise(int op, const u64* a, const u64* b, u64* out, EwGeom g, long long total,
                               Tables tb, const u64* imul_f) {
     pdl_begin();
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+    const long long pairs = total >> 1;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < pairs;
          idx += (long long)gridDim.x * blockDim.x) {
         int item, poly, limb, k;
-        ew_decode(idx, g, item, poly, limb, k);
+        ew_decode(idx << 1, g, item, poly, limb, k);
         const u64 q = tb.q[limb];
         const size_t in_poly = ((size_t)poly * g.L + limb) * g.n + k;
-        const u64 x = a[(size_t)item * g.as + in_poly];
-        u64 r;
+        const ulonglong2 x = ld2(a + (size_t)item * g.as + in_poly);
+        ulonglong2 bv;
         switch (op) {
-            case EW_ADD: r = add_mod(x, b[(size_t)item * g.bs + in_poly], q); break;
-            case EW_SUB: r = sub_mod(x, b[(size_t)item * g.bs + in_poly], q); break;
-            case EW_ADDC: r = poly == 0 ? add_mod(x, b[limb], q) : x; break;
-            case EW_ADDPT: r = poly == 0 ? add_mod(x, b[(size_t)limb * g.n + k], q) : x; break;
-            case EW_REDUCE: r = barrett128(u128v{0, x}, q, tb.br1[limb], tb.br0[limb]); break;
-            default: {
-                const u64 y = op == EW_MULC ? b[limb] : (op == EW_MULPT ? b[(size_t)limb * g.n + k] : imul_f[(size_t)limb * g.n + k]);
-                if (q < NTT_DBL_BOUND) {
-                    const DblC dc{tb.qd[limb], tb.qinvd[limb]};
-                    r = d2u_canon(mulmod_d(u2d(x), u2d(y), dc), dc);
-                } else {
-                    r = mul_mod(x, y, q, tb.br1[limb], tb.br0[limb]);
-                }
-                break;
-            }
+            case EW_ADD:
+            case EW_SUB: bv = ld2(b + (size_t)item * g.bs + in_poly); break;
+            case EW_ADDC:
+            case EW_MULC: bv.x = bv.y = b[limb]; break;
+            case EW_ADDPT:
+            case EW_MULPT: bv = ld2(b + (size_t)limb * g.n + k); break;
+            case EW_REDUCE: bv = make_ulonglong2(0, 0); break;
+            default: bv = ld2(imul_f + (size_t)limb * g.n + k); break;
         }
-        out[(size_t)item * g.os + in_poly] = r;
+        st2(out + (size_t)item * g.os + in_poly, ew_apply(op, x.x, bv.x, poly, q, limb, tb),
+            ew_apply(op, x.y, bv.y, poly, q, limb, tb));
     }
 }
 
@@ -76,7 +89,7 @@ int op_ew(helr_ctx* c, int op, const u64* a, long long as, const u64* b, long lo
     if (count == 0) return HELR_OK;
     EwGeom g{c->n, c->log_n, c->L, level + 1, as, bs, os};
     long long total = (long long)count * 2 * (level + 1) * c->n;
-    int blocks = blocks_for(total, 256);
+    int blocks = blocks_for(total / 2, 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     ProfScope ps(PROF_ELEM, 8.0 * total * ((op == EW_ADD || op == EW_SUB) ? 3 : 2), s);
     if (op == EW_REDUCE) b = a;  // unary
