@@ -157,9 +157,9 @@ def ncu_traffic():
     path = ROOT / "profiles" / "ncu_traffic.json"
     try:
         d = json.loads(path.read_text())
-        return d.get("per_launch", d)
+        return d.get("per_launch", d), (d.get("per_launch_warm") or {})
     except Exception:
-        return {}
+        return {}, {}
 
 
 def max_over_ranks(x: float, ws: int) -> float:
@@ -413,13 +413,15 @@ def main():
     dom = max(range(8), key=lambda i: msa[i])
     peak, peak_kind = peaks()
     achieved = (bya[dom] / cna[dom]) / ((msa[dom] / cna[dom]) / 1000.0) / 1e9
-    traffic = ncu_traffic().get(CATS[dom])
+    traffic_cold, traffic_warm = ncu_traffic()
+    traffic = traffic_cold.get(CATS[dom])
     # the event-bracketed replay serialises the graph (no programmatic
     # dependent-launch overlap), so per-category times add up to more than a
     # step: shares are reported against the attributed sum
     attributed = sum(msa) / args.profile_steps
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu, profiles/ncu_traffic.json)",
+                "traffic_warm_l2": traffic_warm.get(CATS[dom]),
                 "kernel": CATS[dom], "peak_kind": peak_kind,
                 "share_of_step": (msa[dom] / args.profile_steps) / attributed,
                 "attributed_ms_per_step": attributed,

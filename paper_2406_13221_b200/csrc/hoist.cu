@@ -23,6 +23,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+#ifndef HELR_HOIST_EXP
+#define HELR_HOIST_EXP 0  // timing experiments only (wrong results): 1 keys from a cache-resident window, 2 digits likewise
+#endif
 constexpr int HOIST_T = 128;     // threads per block (coefficients per tile)
 #ifndef HELR_HOIST_STAGES
 #define HELR_HOIST_STAGES 3
@@ -90,13 +93,21 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
 #pragma unroll
         for (int w = b; w < 2 * ND; w += NB) {
             const int j = w < ND ? w : w - ND;
+#if HELR_HOIST_EXP & 1
+            cp_async8(slot(stage, w), hk.key[0] + tid + 128 * w);
+#else
             cp_async8(slot(stage, w), kt + (size_t)j * kds + (w < ND ? k0off : k1off));
+#endif
         }
         if (FULL || b < nb) {
 #pragma unroll
             for (int j = 0; j < ND; j++)
+#if HELR_HOIST_EXP & 2
+                cp_async8(slot(stage, 2 * ND + b * ND + j), ext + (src & 1023) + 1024 * (b * ND + j));
+#else
                 cp_async8(slot(stage, 2 * ND + b * ND + j),
                           xb + (size_t)b * ext_item_stride + (size_t)j * ext_digit_stride + src);
+#endif
         }
         if (b == NB - 1) cp_async_commit();
     };

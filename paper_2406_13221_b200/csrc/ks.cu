@@ -201,21 +201,27 @@ __global__ void k_tensor(TensorArgs ta, u64* d, int n, int L, Tables tb) {
     u64* d1 = d0 + (size_t)L * n;
     u64* d2 = d1 + (size_t)L * n;
     if (q < NTT_DBL_BOUND) {  // fp64 limb: exact signed products, one reduction (|sum| < 1.2 q * 2 terms)
+        // two consecutive coefficients per thread (16-byte accesses; n is even)
         const DblC dc{tb.qd[p], tb.qinvd[p]};
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        const size_t ps = (size_t)L * n;
+        for (int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x); i < n; i += 2 * gridDim.x * blockDim.x) {
+            double s0x = 0.0, s1x = 0.0, s2x = 0.0, s0y = 0.0, s1y = 0.0, s2y = 0.0;
             for (int t = 0; t < ta.terms; t++) {
-                const u64* a0 = ta.a + (size_t)it * ta.a_is + (size_t)t * ta.a_ts + (size_t)p * n;
-                const u64* b0 = ta.b + (size_t)it * ta.b_is + (size_t)t * ta.b_ts + (size_t)p * n;
-                const double x0 = u2d(a0[i]), x1 = u2d(a0[(size_t)L * n + i]);
-                const double y0 = u2d(b0[i]), y1 = u2d(b0[(size_t)L * n + i]);
-                s0 = __dadd_rn(s0, mulmod_d(x0, y0, dc));
-                s1 = __dadd_rn(s1, __dadd_rn(mulmod_d(x0, y1, dc), mulmod_d(x1, y0, dc)));
-                s2 = __dadd_rn(s2, mulmod_d(x1, y1, dc));
+                const u64* a0 = ta.a + (size_t)it * ta.a_is + (size_t)t * ta.a_ts + (size_t)p * n + i;
+                const u64* b0 = ta.b + (size_t)it * ta.b_is + (size_t)t * ta.b_ts + (size_t)p * n + i;
+                const ulonglong2 A0 = ld2(a0), A1 = ld2(a0 + ps), B0 = ld2(b0), B1 = ld2(b0 + ps);
+                const double x0 = u2d(A0.x), x1 = u2d(A1.x), y0 = u2d(B0.x), y1 = u2d(B1.x);
+                const double z0 = u2d(A0.y), z1 = u2d(A1.y), w0 = u2d(B0.y), w1 = u2d(B1.y);
+                s0x = __dadd_rn(s0x, mulmod_d(x0, y0, dc));
+                s1x = __dadd_rn(s1x, __dadd_rn(mulmod_d(x0, y1, dc), mulmod_d(x1, y0, dc)));
+                s2x = __dadd_rn(s2x, mulmod_d(x1, y1, dc));
+                s0y = __dadd_rn(s0y, mulmod_d(z0, w0, dc));
+                s1y = __dadd_rn(s1y, __dadd_rn(mulmod_d(z0, w1, dc), mulmod_d(z1, w0, dc)));
+                s2y = __dadd_rn(s2y, mulmod_d(z1, w1, dc));
             }
-            d0[i] = d2u_canon(s0, dc);
-            d1[i] = d2u_canon(s1, dc);
-            d2[i] = d2u_canon(s2, dc);
+            st2(d0 + i, d2u_canon(s0x, dc), d2u_canon(s0y, dc));
+            st2(d1 + i, d2u_canon(s1x, dc), d2u_canon(s1y, dc));
+            st2(d2 + i, d2u_canon(s2x, dc), d2u_canon(s2y, dc));
         }
         return;
     }
@@ -250,7 +256,7 @@ int op_mul_relin_sum(helr_ctx* c, const u64* a, long long a_is, long long a_ts, 
     for (int b0 = 0; b0 < count; b0 += chunk) {
         int nb = count - b0 < chunk ? count - b0 : chunk;
         KsWs w = ks_ws(c, chunk);
-        dim3 g(blocks_for(c->n, 256), level + 1, nb);
+        dim3 g(blocks_for(c->n / 2, 256), level + 1, nb);  // two coefficients per thread on fp64 limbs (grid-stride otherwise)
         TensorArgs ta{a + (size_t)b0 * a_is, a_is, a_ts, b + (size_t)b0 * b_is, b_is, b_ts, terms};
         {
             ProfScope ps(PROF_TENSOR, 8.0 * c->n * nb * (level + 1) * (4.0 * terms + 3.0), s);

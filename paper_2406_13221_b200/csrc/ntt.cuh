@@ -353,10 +353,10 @@ __device__ __forceinline__ int swz128(int e) {  // word index -> swizzled word i
     return (e & ~15) | (((((e >> 1) ^ (e >> 4)) & 7) << 1)) | (e & 1);
 }
 template <int LOG_T, int LOG_R, int COLS, bool IS_COL, bool INV, int S2, bool DBL, class Ld, class St, bool PRE = false,
-          bool TWSM = false>
+          bool TWSM = false, bool TWFILL = false>
 __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Tables& tb, const LimbMap& map,
                                          const NttPassArgs& a, u64* sm, const int bx, const int li, const int z,
-                                         const double* tws = nullptr) {
+                                         double* tws = nullptr) {
     using S = NttShape<LOG_T, LOG_R>;
     constexpr int T = S::T, R = S::R, NG = S::NG;
     constexpr int TPS = T / R;  // threads per sub-transform
@@ -387,6 +387,7 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
     // every column) are staged in shared memory by the kernel, so the
     // per-stage twiddle reads are LDS instead of LDG queued behind the data
     // loads and stores (kColTwSmem)
+    const double* WDG = WD;  // the limb's table in global memory
     if constexpr (TWSM) WD = tws;
     int cc, s;
     if (IS_COL) { cc = tid % COLS; s = tid / COLS; }
@@ -540,6 +541,12 @@ __device__ __forceinline__ void ntt_body(const Ld& ld, const St& st, const Table
             } else {
 #pragma unroll
                 for (int i = 0; i < R; i++) x[i] = in_v(LD(base + (i << lo)));
+            }
+            if constexpr (TWFILL) {
+                // the twiddle table is fetched AFTER the tile's loads were
+                // issued, so its latency and the barrier overlap with them
+                if (tid < T) tws[tid] = __ldg(WDG + tid);
+                __syncthreads();
             }
             if constexpr (DBL) {
                 if (!raw_in) {
@@ -716,16 +723,10 @@ ntt_pass(Ld ld, St st, Tables tb, LimbMap map, NttPassArgs a) {
     constexpr bool TWS = kColTwSmem && IS_COL && LOG_T >= 6 && ((1 << LOG_T) <= (1 << LOG_T) * COLS / (1 << LOG_R));
     __shared__ __align__(16) double tws[TWS ? T : 1];
     if (tb.q[map.prime[li]] < NTT_DBL_BOUND) {
-        const double* twp = nullptr;
-        if constexpr (TWS) {
-            // one coalesced read of the limb's column-pass table per CTA
-            const int prime = map.prime[li];
-            if (threadIdx.x < T)
-                tws[threadIdx.x] = __ldg((INV ? tb.itwd : tb.twd) + ((size_t)prime << a.log_n) + threadIdx.x);
-            __syncthreads();
-            twp = tws;
-        }
-        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true, Ld, St, false, TWS>(ld, st, tb, map, a, sm, blockIdx.x, li, z, twp);
+        // column passes: one coalesced read of the limb's 2^LOG_T-entry table
+        // per CTA, issued by the body behind its tile loads (TWFILL)
+        ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, true, Ld, St, false, TWS, TWS>(ld, st, tb, map, a, sm, blockIdx.x, li, z,
+                                                                                     tws);
     } else
         ntt_body<LOG_T, LOG_R, COLS, IS_COL, INV, S2, false>(ld, st, tb, map, a, sm, blockIdx.x, li, z);
 }

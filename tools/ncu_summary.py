@@ -96,6 +96,8 @@ def main():
     ap.add_argument("csv")
     ap.add_argument("--md", default=None)
     ap.add_argument("--traffic", default=None)
+    ap.add_argument("--warm", default=None,
+                    help="second launch list of the same step captured with --cache-control none (L2 kept warm)")
     ap.add_argument("--title", default="ncu launch list")
     a = ap.parse_args()
     launches = load(a.csv)
@@ -129,10 +131,21 @@ def main():
         per_launch = dict(per_kernel)
         if cats["ntt"]["has_dram"] and (n_pass or n_cl):
             per_launch["ntt"] = cats["ntt"]["dram"] / (n_pass / 2.0 + n_cl)
-        tr = {"per_launch": per_launch, "per_kernel_launch": per_kernel,
+        warm = None
+        if a.warm:
+            wl = load(a.warm)
+            wc, _ = summarise(wl)
+            warm = {c: s["dram"] / s["launches"] for c, s in wc.items() if s["launches"] and s["has_dram"]}
+            wp = sum(1 for d in wl if "ntt_pass" in d["name"])
+            wcl = sum(1 for d in wl if "ntt_cluster" in d["name"])
+            if wc["ntt"]["has_dram"] and (wp or wcl):
+                warm["ntt"] = wc["ntt"]["dram"] / (wp / 2.0 + wcl)
+        tr = {"per_launch": per_launch, "per_launch_warm": warm, "per_kernel_launch": per_kernel,
               "ntt_transforms": n_pass / 2.0 + n_cl, "_source": a.csv,
               "_unit": "DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum, ncu serialised, cold cache); "
-                       "per_launch: per library launch (NTT: per two-pass transform), per_kernel_launch: per CUDA kernel"}
+                       "per_launch: per library launch (NTT: per two-pass transform), per_kernel_launch: per CUDA kernel; "
+                       "per_launch_warm: the same from a capture with --cache-control none (L2 not flushed between "
+                       "kernels, as in the real step)"}
         with open(a.traffic, "w") as fh:
             json.dump(tr, fh, indent=1)
 
