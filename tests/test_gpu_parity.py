@@ -127,6 +127,13 @@ def test_elementwise(pair, rng):
     out = ctx._ct_buffer()
     _lib.call("helr_mul_plain", ctx.handle, a.data.data_ptr(), pt.data_ptr(), out.data_ptr(), 1, lvl, stream())
     np.testing.assert_array_equal(u64(out)[:, : lvl + 1], orc.mul_plain(ref[0:1], opt, lvl)[0][:, : lvl + 1])
+    # vector cadd (hesim.py:177-184): the plaintext is added to c0 only, residue for residue
+    out = ctx._ct_buffer()
+    _lib.call("helr_add_plain", ctx.handle, a.data.data_ptr(), pt.data_ptr(), out.data_ptr(), 1, lvl, stream())
+    exp = ref[0].copy()
+    for p in range(lvl + 1):
+        exp[0, p] = (exp[0, p] + opt[p]) % np.uint64(P.q[p])
+    np.testing.assert_array_equal(u64(out)[:, : lvl + 1], exp[:, : lvl + 1])
     out = ctx._ct_buffer()
     _lib.call("helr_imul", ctx.handle, a.data.data_ptr(), out.data_ptr(), 1, lvl, stream())
     np.testing.assert_array_equal(u64(out), orc.imul(ref[0:1], lvl)[0])
