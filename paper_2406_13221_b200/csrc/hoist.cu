@@ -31,6 +31,10 @@ constexpr int HOIST_T = 128;     // threads per block (coefficients per tile)
 #define HELR_HOIST_STAGES 3
 #endif
 constexpr int HOIST_STAGES = HELR_HOIST_STAGES;  // steps in flight per thread
+#ifndef HELR_HOIST_KEYREG
+#define HELR_HOIST_KEYREG 0  // 1: key words bypass shared memory (ld.global.nc into registers one step ahead)
+#endif
+constexpr bool HOIST_KEYREG = HELR_HOIST_KEYREG;
 
 
 // grid: x = coefficient tile * chunks + chunk (chunks of NB ciphertexts share
@@ -62,7 +66,8 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
     const int n = A.n, log_n = A.log_n, nl = A.nl, K = A.K, L = A.L, LK = A.LK, B = A.B, nchunks = A.nchunks,
               fold = A.fold;
     const u64* one_sh = A.one_sh;
-    constexpr int W = (2 + NB) * ND;  // words per thread per stage
+    constexpr int KW = HOIST_KEYREG ? 0 : 2 * ND;  // key words staged in shared memory
+    constexpr int W = KW + NB * ND;                 // words per thread per stage
     constexpr int S = HOIST_STAGES;
     extern __shared__ u64 hsm[];
     const int tid = threadIdx.x;
@@ -91,7 +96,7 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
         if (b == 0) src = galois_perm_e(ei, (u64)hk.gal[tc], log_n);
         const u64* kt = hk.key[tc];
 #pragma unroll
-        for (int w = b; w < 2 * ND; w += NB) {
+        for (int w = b; w < KW; w += NB) {
             const int j = w < ND ? w : w - ND;
 #if HELR_HOIST_EXP & 1
             cp_async8(slot(stage, w), hk.key[0] + tid + 128 * w);
@@ -103,9 +108,9 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
 #pragma unroll
             for (int j = 0; j < ND; j++)
 #if HELR_HOIST_EXP & 2
-                cp_async8(slot(stage, 2 * ND + b * ND + j), ext + (src & 1023) + 1024 * (b * ND + j));
+                cp_async8(slot(stage, KW + b * ND + j), ext + (src & 1023) + 1024 * (b * ND + j));
 #else
-                cp_async8(slot(stage, 2 * ND + b * ND + j),
+                cp_async8(slot(stage, KW + b * ND + j),
                           xb + (size_t)b * ext_item_stride + (size_t)j * ext_digit_stride + src);
 #endif
         }
@@ -127,6 +132,20 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
     for (int t = 0; t < S - 1; t++) issue(t);
     int run = 0;
     static_assert(S >= 2, "the prefetch needs at least two stages");
+    // HOIST_KEYREG: this step's key words were loaded into registers during the
+    // previous step (coalesced ld.global.nc), the next step's are requested
+    // before this step's arithmetic starts
+    u64 kn[2 * ND], kn2[2 * ND];  // key words of steps t + 1 and t + 2
+    auto load_keys = [&](int t, u64 (&dst)[2 * ND]) {
+        const int tc = t < hk.nsteps ? t : hk.nsteps - 1;
+        const u64* kt = hk.key[tc];
+#pragma unroll
+        for (int w = 0; w < 2 * ND; w++) {
+            const int j = w < ND ? w : w - ND;
+            dst[w] = __ldg(kt + (size_t)j * kds + (w < ND ? k0off : k1off));
+        }
+    };
+    if constexpr (HOIST_KEYREG) { load_keys(0, kn); load_keys(1, kn2); }
     for (int t = 0; t < hk.nsteps; t++) {
         // step t's words have landed (step t + 1 may still be in flight); they
         // are read into registers first and step t + S - 1 is issued AFTER
@@ -137,12 +156,18 @@ __device__ __forceinline__ void hoist_body(const HoistKeys& hk, const HoistArgs&
         cp_async_wait<S - 2>();
         const int stage = t % S;
         u64 kw[2 * ND], dw[NB * ND];
+        if constexpr (HOIST_KEYREG) {
 #pragma unroll
-        for (int j = 0; j < 2 * ND; j++) kw[j] = *slot(stage, j);
+            for (int j = 0; j < 2 * ND; j++) { kw[j] = kn[j]; kn[j] = kn2[j]; }
+            load_keys(t + 2, kn2);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 2 * ND; j++) kw[j] = *slot(stage, j);
+        }
 #pragma unroll
         for (int b = 0; b < NB; b++) {
 #pragma unroll
-            for (int j = 0; j < ND; j++) dw[b * ND + j] = (FULL || b < nb) ? *slot(stage, 2 * ND + b * ND + j) : 0;
+            for (int j = 0; j < ND; j++) dw[b * ND + j] = (FULL || b < nb) ? *slot(stage, KW + b * ND + j) : 0;
         }
         int nsrc = 0;
         if constexpr (DBL) {
@@ -502,7 +527,7 @@ static int hoist_fold(const helr_ctx* c, int nd) {
 template <int ND, int NB>
 static void launch_hoisted_nb(dim3 g, cudaStream_t s, const HoistKeys& hk, HoistArgs A, const Tables& tb) {
     A.nchunks = (A.B + NB - 1) / NB;
-    const size_t smem = sizeof(u64) * (size_t)HOIST_STAGES * (2 + NB) * ND * HOIST_T;
+    const size_t smem = sizeof(u64) * (size_t)HOIST_STAGES * ((HOIST_KEYREG ? 0 : 2) + NB) * ND * HOIST_T;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_ks_inner_hoisted<ND, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
