@@ -50,14 +50,16 @@ bool pdl_enabled() {
 // transforms per launch that take the cluster path
 bool ntt_cluster_enabled(long long limb_transforms) {
     static int on = -1;
-    static long long lo = 1;
+    static long long lo = 1, hi = 1ll << 40;
     if (on < 0) {
         const char* e = getenv("HELR_NTT_CLUSTER");
         on = e ? (atoi(e) != 0) : 0;  // measured slower than the two-pass kernels
         const char* m = getenv("HELR_NTT_CL_MIN");
         lo = m ? atoll(m) : 1;
+        const char* x = getenv("HELR_NTT_CL_MAX");  // e.g. only the small single-ciphertext launches
+        hi = x ? atoll(x) : (1ll << 40);
     }
-    return on != 0 && limb_transforms >= lo;
+    return on != 0 && limb_transforms >= lo && limb_transforms <= hi;
 }
 // cp.async.bulk for the dense tile of the cluster NTT (HELR_NTT_BULK=0: plain loads / stores)
 bool ntt_bulk_enabled() {
